@@ -1,0 +1,180 @@
+"""CPU oracle for the MoA reshape-transpose FFT -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` leg may import this package.  The product path
+(``paper_0811_2535_b200``) never imports it and shares no code with it.
+
+Thin ctypes wrapper over ``oracle/moa_oracle.c`` (plain C, built with
+``-O2 -ffp-contract=off -fno-fast-math -fopenmp``).  Each function names the
+paper figure it follows (P:<line> of PAPER.md, arXiv 0811.2535):
+
+* ``fft``       -- Fig 2.1 in the Fig 3.9 in-place form;
+                   ``threads > 1`` is the Fig 6.1 ``parallel do`` template
+* ``fft_temp``  -- Fig 3.8, temporary ``xx``
+* ``dft``       -- the plain definition X_k = sum_j x_j w^{jk}, O(n^2), long double
+* ``bitrev``    -- P_n, Fig 2.1 line 1
+* ``weights``   -- weight(row) = EXP(sign 2 pi i row / L) (Fig 3.8)
+* ``dist_sim``  -- Fig 5.7 + Fig 5.9 with m virtual processors
+* ``gamma``     -- row-major offset, Def A.1
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "moa_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+          "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library in-tree (gcc); returns its path."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            dp = ctypes.POINTER(ctypes.c_double)
+            i64 = ctypes.c_int64
+            lib.oracle_fft.argtypes = [i64, ctypes.c_int, ctypes.c_int, dp, dp]
+            lib.oracle_fft_temp.argtypes = [i64, ctypes.c_int, dp, dp]
+            lib.oracle_dft.argtypes = [i64, ctypes.c_int, dp, dp]
+            lib.oracle_bitrev.argtypes = [i64, dp, dp]
+            lib.oracle_weights.argtypes = [i64, ctypes.c_int, dp]
+            lib.oracle_omega.argtypes = [i64, i64, ctypes.c_int, dp]
+            lib.oracle_omega.restype = None
+            lib.oracle_rev.argtypes = [i64, ctypes.c_int]
+            lib.oracle_rev.restype = i64
+            lib.oracle_dist_sim.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp,
+                                            dp, ctypes.POINTER(i64)]
+            lib.oracle_gamma.argtypes = [ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+            lib.oracle_gamma.restype = i64
+            lib.oracle_max_threads.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise ValueError(f"oracle {what} failed with code {rc}")
+
+
+def fft(x, sign: int = -1, threads: int = 1) -> np.ndarray:
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_fft(x.size, sign, threads, _dp(x), _dp(out)), "fft")
+    return out
+
+
+def fft_temp(x, sign: int = -1) -> np.ndarray:
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_fft_temp(x.size, sign, _dp(x), _dp(out)), "fft_temp")
+    return out
+
+
+def dft(x, sign: int = -1) -> np.ndarray:
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_dft(x.size, sign, _dp(x), _dp(out)), "dft")
+    return out
+
+
+def bitrev(x) -> np.ndarray:
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_bitrev(x.size, _dp(x), _dp(out)), "bitrev")
+    return out
+
+
+def rev(j: int, t: int) -> int:
+    return int(_load().oracle_rev(j, t))
+
+
+def weights(L: int, sign: int = -1) -> np.ndarray:
+    out = np.empty(max(L // 2, 1), dtype=np.complex128)
+    _check(_load().oracle_weights(L, sign, _dp(out)), "weights")
+    return out[: L // 2]
+
+
+def omega(e: int, L: int, sign: int = -1) -> complex:
+    out = np.empty(1, dtype=np.complex128)
+    _load().oracle_omega(e, L, sign, _dp(out))
+    return complex(out[0])
+
+
+def dist_sim(x, m: int, breakpoint: int | None = None, sign: int = -1):
+    """Fig 5.7/5.9 simulation.  Returns (xcyclic[m, psize], gathered X[n], counts dict).
+
+    breakpoint defaults to the high end log2(psize)+1 (reading R6)."""
+    x = _c128(x)
+    n = x.size
+    psize = n // m
+    if breakpoint is None:
+        breakpoint = int(psize).bit_length()  # log2(psize) + 1
+    cyc = np.empty(n, dtype=np.complex128)
+    out = np.empty(n, dtype=np.complex128)
+    counts = (ctypes.c_int64 * 4)()
+    _check(_load().oracle_dist_sim(n, m, breakpoint, sign, _dp(x), _dp(cyc), _dp(out), counts),
+           "dist_sim")
+    c = {"messages": counts[0], "elements_per_message": counts[1],
+         "weights_per_proc": counts[2], "assigns_per_stage": counts[3]}
+    return cyc.reshape(m, psize), out, c
+
+
+def gamma(shape, index) -> int:
+    d = len(shape)
+    s = (ctypes.c_int64 * d)(*shape)
+    i = (ctypes.c_int64 * d)(*index)
+    return int(_load().oracle_gamma(d, s, i))
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def l2_parts(got, ref, chunk: int = 1 << 22):
+    """(sum |g-o|^2, sum |o|^2) accumulated in long double, chunked so 2^30 fits in RAM."""
+    g = np.asarray(got, dtype=np.complex128).reshape(-1).view(np.float64)
+    o = np.asarray(ref, dtype=np.complex128).reshape(-1).view(np.float64)
+    if g.shape != o.shape:
+        raise ValueError(f"shape mismatch {g.shape} vs {o.shape}")
+    num = np.longdouble(0)
+    den = np.longdouble(0)
+    for s in range(0, g.size, chunk):
+        gg = g[s:s + chunk].astype(np.longdouble)
+        oo = o[s:s + chunk].astype(np.longdouble)
+        num += np.sum((gg - oo) ** 2)
+        den += np.sum(oo ** 2)
+    return num, den
+
+
+def rel_l2(got, ref) -> float:
+    """relL2 = ||g - o||_2 / ||o||_2 accumulated in long double."""
+    num, den = l2_parts(got, ref)
+    return float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num))
