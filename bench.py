@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the MoA reshape-transpose FFT on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--t 24]
+
+A step is one complete forward complex128 FFT of n = 2^t (default t = 24,
+BASELINE.json configs[2], the size the metric's >= 60 % HBM target is quoted
+on), inputs resident in HBM, through the C ABI (moa_fft_execute).  With N > 1
+(torchrun, one rank per GPU, NCCL) the same transform is partitioned p = N
+ways (reshape-transpose with one all-to-all): strong scaling.
+
+metric  = GFLOP/s counted as 5 n log2 n per transform (BASELINE.json metric)
+roofline= the dominant kernel's algorithmic bytes / its event-timed launch
+          duration against MEASURED_PEAKS.json hbm_gbs
+e2e     = same metric through moa_fft_execute_host (pinned host in/out,
+          H2D + transform + D2H inside the timed region)
+cpu_baseline / --impl reference = the CPU oracle (oracle/, Fig 3.9 + Fig 6.1
+          OpenMP mode) timed on this host's cores -- a baseline, not the target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "complex128 1-D FFT GFLOP/s (5n log2 n) and HBM GB/s fraction, 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+
+
+def flops(n: int) -> float:
+    return 5.0 * n * (n.bit_length() - 1)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel_name: str, n: int, p: int):
+    """dram bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{kernel_name}|n={n}|p={p}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML polling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - NVML missing
+            self.err = str(e)
+
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for bit, name in self.REASONS.items():
+            if r & bit and name != "gpu_idle":
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._h is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._h is not None:
+            self._stop.set()
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(t: int, reps: int):
+    """The oracle as it stands (Fig 3.9; Fig 6.1 parallel-do mode on all host cores)."""
+    import moa_inputs
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    x = moa_inputs.signal_for(t)
+    oracle.fft(x[:1 << 10], -1, threads=cores)  # load + build
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.fft(x, -1, threads=cores)
+    dt = (time.perf_counter() - t0) / reps
+    return flops(1 << t) / dt / 1e9, cores, dt
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the CPU oracle on this host, same config/metric (rank 0 only)."""
+    if rank != 0:
+        return
+    import moa_inputs
+    import oracle
+    t = args.t
+    n = 1 << t
+    cores = len(os.sched_getaffinity(0))
+    x = moa_inputs.signal_for(t)
+    for _ in range(args.warmup):
+        oracle.fft(x, -1, threads=cores)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.fft(x, -1, threads=cores)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = args.steps * flops(n) / total / 1e9
+    sample = f"each step = one full n=2^{t} oracle transform (Fig 3.9 radix-2, Fig 6.1 OpenMP mode)"
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(t, world, None),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample, "cpu": cpu_model()},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(t: int, world: int, info):
+    c = {"workload": f"fft1d_c2c_forward_n2^{t}", "n": 1 << t, "p": world,
+         "input": "i.i.d. uniform [-1,1) re/im, SplitMix64 seed 0x08112535+t",
+         "parallelism": (f"reshape-transpose p={world} (NCCL all-to-all)" if world > 1 else "single GPU"),
+         "l2": "working set (in + out + scratch = 768 MiB at 2^24) larger than the 126 MB L2; no flush"}
+    if info is not None:
+        c["lift"] = info["lift"]
+        c["passes"] = info["passes"]
+    return c
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank: int, world: int):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import moa_inputs
+    import paper_0811_2535_b200 as moa
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    t = args.t
+    n = 1 << t
+    if world > 1:
+        moa.dist_init()
+    M = n // world
+    x = torch.empty(M, dtype=torch.complex128, device=dev)
+    moa.gen_uniform(moa_inputs.seed_for(t), M, x, first=rank, stride=world)
+    out = torch.empty_like(x)
+    stream = torch.cuda.Stream(device=dev)
+    plan = moa.Plan(n, world, -1, stream=stream)
+    info = plan.info()
+    lib = moa.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            plan.execute(x, out)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-kernel events on the plan stream
+    lib.moa_fft_set_profiling(plan._h, 1)
+    stats_buf = (moa_stat * 16)()
+    lib.moa_fft_get_profile(plan._h, stats_buf, 16)  # reset
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(dev.index)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.execute(x, out)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    nstat = lib.moa_fft_get_profile(plan._h, stats_buf, 16)
+    lib.moa_fft_set_profiling(plan._h, 0)
+    if world > 1:
+        tt = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    value = args.steps * flops(n) / elapsed / 1e9
+    kstats = [{"name": stats_buf[i].name.decode(), "launches": stats_buf[i].launches,
+               "avg_us": stats_buf[i].total_ms * 1e3 / max(1, stats_buf[i].launches),
+               "alg_bytes": int(stats_buf[i].alg_bytes)} for i in range(nstat)]
+    kernel_total = sum(k["avg_us"] * k["launches"] for k in kstats if "NCCL" not in k["name"])
+    kern = [k for k in kstats if "NCCL" not in k["name"]]
+    dom = max(kern, key=lambda k: k["avg_us"] * k["launches"])
+    peaks = measured_peaks()
+    achieved = dom["alg_bytes"] / (dom["avg_us"] * 1e-6) / 1e9
+    traffic = ncu_traffic(dom["name"], n, world)
+    roofline = {"bound": "hbm", "kernel": dom["name"], "achieved": round(achieved, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "traffic": traffic, "peak_source": peaks["source"],
+                "share_of_step": round(dom["avg_us"] * dom["launches"] / max(kernel_total, 1e-9), 3)}
+
+    # ---- end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.from_numpy(moa_inputs.complex_signal(moa_inputs.seed_for(t), M, first=rank,
+                                                         stride=world)).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        for _ in range(max(1, min(args.warmup, 2))):
+            plan.execute_host(hin, hout)
+        barrier()
+        e_steps = max(1, min(args.steps, 10))
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(e_steps):
+            plan.execute_host(hin, hout)
+        t1.record(stream)
+        t1.synchronize()
+        e_el = t0.elapsed_time(t1) * 1e-3
+        if world > 1:
+            tt = torch.tensor([e_el], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_el = float(tt.item())
+        e2e = {"value": round(e_steps * flops(n) / e_el / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hin.numel() * 16), "d2h_bytes_per_step": int(hout.numel() * 16),
+               "steps": e_steps, "ms_per_step": round(e_el / e_steps * 1e3, 3)}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            rate, cores, dt = cpu_oracle_rate(t, args.cpu_reps)
+            cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{args.cpu_reps} full n=2^{t} oracle transforms ({dt:.2f} s each)",
+                   "cpu": cpu_model()}
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_block(t, world, info),
+                "hbm": {"alg_bytes_per_step": int(info["hbm_bytes"]),
+                        "alg_GBps": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9, 1),
+                        "frac_of_measured": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9
+                                                  / peaks["hbm_gbs"], 4)},
+                "roofline": roofline, "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(args.steps * info["launches"]),
+                "clocks": sampler.summary()}
+        if world > 1:
+            a2a = [k for k in kstats if "NCCL" in k["name"]]
+            if a2a:
+                bw = a2a[0]["alg_bytes"] / (a2a[0]["avg_us"] * 1e-6) / 1e9
+                line["a2a"] = {"GBps_per_rank": round(bw, 1), "frac_of_770": round(bw / 770.0, 4),
+                               "avg_us": round(a2a[0]["avg_us"], 2)}
+        print(json.dumps(line), flush=True)
+    plan.destroy()
+    if world > 1:
+        moa.dist_finalize()
+
+
+class moa_stat(__import__("ctypes").Structure):
+    import ctypes as _c
+    _fields_ = [("name", _c.c_char * 64), ("launches", _c.c_int), ("total_ms", _c.c_double),
+                ("alg_bytes", _c.c_int64)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--t", type=int, default=24)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

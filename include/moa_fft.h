@@ -1,0 +1,176 @@
+/*
+ * moa_fft.h -- C ABI of the B200-native MoA reshape-transpose FFT.
+ *
+ * The operation (PAPER.md = arXiv 0811.2535, cited P:<line>):
+ *   Input x in C^n, n = 2^t, t >= 1; output the FFT of x            (Fig 2.1)
+ *   X_k = sum_{j<n} x_j exp(sign * 2*pi*i * j*k / n), no normalisation
+ *   computed as the radix-2 Cooley-Tukey FFT of Fig 2.1 / Fig 3.9 (P:103-117,
+ *   P:314-333) restructured by dimension lifting ("reshape-transpose"):
+ *   local butterfly passes, twiddle scaling, a transpose, more local passes;
+ *   and for p > 1 the block/cyclic partition of §4-§5 (Fig 4.9 P:706-747,
+ *   Fig 5.7) with the single block->cyclic redistribution of
+ *   Fig 5.9 done as an NCCL all-to-all.
+ *
+ * Data: complex128 = two IEEE doubles (re, im) interleaved, 16-byte aligned,
+ * i.e. torch.complex128 / std::complex<double> / double2.
+ *
+ * Every pointer argument called `in` / `out` in an execute call is a
+ * caller-owned DEVICE pointer on the plan's device unless the function name
+ * says _host.  The library never frees caller memory.  No function here takes
+ * or returns a torch type.  All functions are thread-compatible (one plan per
+ * thread at a time); the error message is thread-local.
+ *
+ * Errors: functions returning int return MOA_OK (0) or a negative MOA_ERR_*
+ * code; functions returning a plan return NULL on error.  After any error,
+ * moa_fft_last_error() describes it (naming the violated bound for argument
+ * errors, as SPEC S:266-274 asks of validate_config).
+ */
+#ifndef MOA_FFT_H
+#define MOA_FFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MOA_OK = 0,
+    MOA_ERR_INVALID_N = -1,    /* n is not 2^t with 1 <= t <= 34                       */
+    MOA_ERR_INVALID_P = -2,    /* p not a power of two, p != world size, or n/p < p */
+    MOA_ERR_INVALID_SIGN = -3, /* sign not -1 or +1                                    */
+    MOA_ERR_ALIGN = -4,        /* a device pointer is NULL or not 16-byte aligned        */
+    MOA_ERR_NO_DIST = -5,      /* p > 1 (real ranks) without moa_dist_init               */
+    MOA_ERR_OOM = -6,          /* device or host allocation failed                     */
+    MOA_ERR_CUDA = -7,         /* a CUDA runtime call or kernel launch failed           */
+    MOA_ERR_NCCL = -8,         /* libnccl missing or an NCCL call failed                */
+    MOA_ERR_INVALID_ARG = -9   /* NULL plan, bad option, or wrong plan kind for the call */
+};
+
+typedef struct moa_fft_plan_s *moa_fft_plan_t;
+
+/* Execution modes (moa_fft_options.mode). */
+enum {
+    MOA_MODE_LIFTED = 0,   /* d(n) lifted passes: the product path  */
+    MOA_MODE_LITERAL = 1,  /* the paper's own schedule on the GPU: bit reversal kernel
+                              (P_n) + t radix-2 stage kernels (Fig 3.9 butterflies,
+                              P:321-327).  Ablation baseline; p == 1 only.               */
+    MOA_MODE_EMULATED = 2  /* p > 1 virtual ranks on this one GPU: the same per-rank
+                              kernels, the all-to-all done with device copies (tests)    */
+};
+
+typedef struct {
+    int mode;            /* MOA_MODE_*                                                */
+    int nlift;           /* 0 = default lifting; else number of factors in lift[]      */
+    int64_t lift[4];     /* lifting <F1..Fd> (powers of two, product n (p=1) or n/p)   */
+    int chunks;          /* p > 1: all-to-all chunks G (0 = default)                   */
+} moa_fft_options;
+
+typedef struct {
+    int64_t n;           /* transform length                                          */
+    int t;               /* log2 n                                                    */
+    int p;               /* ranks the transform is partitioned over (paper's m)        */
+    int rank;            /* this process's rank (0 for p == 1 or emulated)             */
+    int sign;            /* -1 forward / +1 the paper's literal EXP(+2 pi i ...)        */
+    int mode;            /* MOA_MODE_*                                                */
+    int64_t local_n;     /* elements per rank: n / p (the paper's psize)               */
+    int passes;          /* kernel passes over the local data (lifting depth d)       */
+    int64_t lift[4];     /* lifting factors <F1..Fd>                                  */
+    int breakpoint;      /* q at which the cyclic phase starts: log2(psize)+1  */
+    int chunks;          /* all-to-all chunks G                                       */
+    int launches;        /* kernels one execute launches (not counting NCCL's)        */
+    int64_t workspace_bytes;  /* device bytes the plan owns                            */
+    int64_t hbm_bytes;        /* algorithmic HBM bytes per execute on this rank        */
+    int64_t a2a_bytes;        /* bytes this rank sends per execute (p > 1)             */
+} moa_fft_info;
+
+/*
+ * Create a plan for an n-point transform over p ranks.
+ *   n    = 2^t, 1 <= t <= 34 (Fig 2.1 input "n = 2^t, t >= 1").
+ *   p    = 1, or the world size given to moa_dist_init (a power of two, the paper's m)
+ *          with n/p >= p (psize >= m).
+ *   sign = -1 (forward, conventional) or +1 (the paper's literal EXP(+2*pi*i*row/L)).
+ * Binds to the current CUDA device; owns twiddle tables, scratch and (p > 1)
+ * send/receive buffers.  For p > 1 the call is collective.  NULL on error.
+ */
+moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign);
+
+/* As moa_fft_plan with explicit options (NULL = defaults).  A lifting whose
+ * product is wrong or with a factor outside [2, 8192] is MOA_ERR_INVALID_ARG. */
+moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options *opts);
+
+/*
+ * Execute the transform, asynchronously on the plan's stream.
+ *   p == 1: in/out hold n elements in natural order; in == out allowed; in is
+ *           not modified when in != out.
+ *   p > 1 : in/out hold n/p elements of THIS rank in the cyclic layout
+ *           in[j] = x[rank + p*j], out[i] = X[rank + p*i] (the paper's xcyclic,
+ *           P:799).  Collective: every rank calls it in the same order.
+ *   EMULATED plans: in/out hold all p ranks' slices back to back (p*(n/p)).
+ * Returns MOA_OK or MOA_ERR_ALIGN / MOA_ERR_CUDA / MOA_ERR_NCCL.
+ */
+int moa_fft_execute(moa_fft_plan_t plan, const void *in, void *out);
+
+/*
+ * End-to-end form: in/out are HOST pointers (pinned for full speed).  Copies
+ * in -> device, executes, copies the result back, and synchronises the plan
+ * stream before returning.  Same layouts as moa_fft_execute.
+ */
+int moa_fft_execute_host(moa_fft_plan_t plan, const void *host_in, void *host_out);
+
+/* Free everything the plan owns (synchronises its stream first).  NULL-safe. */
+void moa_fft_destroy(moa_fft_plan_t plan);
+
+/* Order the plan's work on `stream` (a cudaStream_t; NULL = legacy default stream). */
+int moa_fft_set_stream(moa_fft_plan_t plan, void *stream);
+
+/* Fill *out with the plan's shape, lifting and byte counts. */
+int moa_fft_plan_info(moa_fft_plan_t plan, moa_fft_info *out);
+
+/*
+ * Per-kernel timing for benchmarks.  While enabled, every kernel an execute
+ * launches is bracketed by a CUDA event pair on the plan's stream.
+ * moa_fft_get_profile synchronises the stream, aggregates the elapsed times per
+ * kernel slot since the last call (then resets), and returns the number of
+ * slots written (<= max_stats), or a negative error code.
+ */
+typedef struct {
+    char name[64];              /* e.g. "pass1 fft_pass<F=4096,T=2>", "pcombine<P=8>"     */
+    int launches;               /* launches aggregated into this slot                      */
+    double total_ms;            /* summed event-measured duration                          */
+    int64_t alg_bytes;          /* algorithmic HBM bytes per launch (read + write)         */
+} moa_fft_kernel_stat;
+
+int moa_fft_set_profiling(moa_fft_plan_t plan, int enable);
+int moa_fft_get_profile(moa_fft_plan_t plan, moa_fft_kernel_stat *stats, int max_stats);
+
+/* Thread-local description of the last error ("" if none). */
+const char *moa_fft_last_error(void);
+
+/*
+ * Distributed setup: one library-owned NCCL communicator per process, created
+ * with ncclCommInitRank from a 128-byte ncclUniqueId that rank 0 obtained with
+ * moa_dist_unique_id and broadcast (the Python side uses torch.distributed).
+ * libnccl.so.2 is resolved at run time (the copy already loaded in the process,
+ * else the path in $MOA_NCCL_LIB, else the loader's search path).
+ */
+int moa_dist_unique_id(void *id_out_128B);
+int moa_dist_init(int rank, int p, const void *id_128B);
+int moa_dist_finalize(void);
+
+/*
+ * Test/bench helper (not part of the transform): fill `count` complex128 values
+ * at device pointer out with x_g = u(seed, 2g) + i*u(seed, 2g+1),
+ * g = first + stride*i, u = SplitMix64 mapped to [-1, 1) (the recipe of
+ * moa_inputs.py; bit-identical to it).  stream may be NULL.
+ */
+int moa_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int64_t count,
+                    void *out, void *stream);
+
+/* Library version string. */
+const char *moa_fft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOA_FFT_H */

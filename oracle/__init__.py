@@ -12,6 +12,7 @@ paper figure it follows (P:<line> of PAPER.md, arXiv 0811.2535):
                    ``threads > 1`` is the Fig 6.1 ``parallel do`` template
 * ``fft_temp``  -- Fig 3.8, temporary ``xx``
 * ``dft``       -- the plain definition X_k = sum_j x_j w^{jk}, O(n^2), long double
+* ``dft_bins``  -- the same definition at selected bins (sampled parity at large n)
 * ``bitrev``    -- P_n, Fig 2.1 line 1
 * ``weights``   -- weight(row) = EXP(sign 2 pi i row / L) (Fig 3.8)
 * ``dist_sim``  -- Fig 5.7 + Fig 5.9 with m virtual processors
@@ -56,6 +57,7 @@ def _load():
             lib.oracle_fft.argtypes = [i64, ctypes.c_int, ctypes.c_int, dp, dp]
             lib.oracle_fft_temp.argtypes = [i64, ctypes.c_int, dp, dp]
             lib.oracle_dft.argtypes = [i64, ctypes.c_int, dp, dp]
+            lib.oracle_dft_bins.argtypes = [i64, ctypes.c_int, dp, i64, ctypes.POINTER(i64), dp]
             lib.oracle_bitrev.argtypes = [i64, dp, dp]
             lib.oracle_weights.argtypes = [i64, ctypes.c_int, dp]
             lib.oracle_omega.argtypes = [i64, i64, ctypes.c_int, dp]
@@ -102,6 +104,18 @@ def dft(x, sign: int = -1) -> np.ndarray:
     x = _c128(x)
     out = np.empty_like(x)
     _check(_load().oracle_dft(x.size, sign, _dp(x), _dp(out)), "dft")
+    return out
+
+
+def dft_bins(x, ks, sign: int = -1) -> np.ndarray:
+    """X_k of the plain definition at the listed bins only (any power-of-two n)."""
+    x = _c128(x)
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int64))
+    out = np.empty(ks.size, dtype=np.complex128)
+    lib = _load()
+    rc = lib.oracle_dft_bins(x.size, sign, _dp(x), ks.size,
+                             ks.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(out))
+    _check(rc, "dft_bins")
     return out
 
 
@@ -160,8 +174,8 @@ def max_threads() -> int:
 
 def l2_parts(got, ref, chunk: int = 1 << 22):
     """(sum |g-o|^2, sum |o|^2) accumulated in long double, chunked so 2^30 fits in RAM."""
-    g = np.asarray(got, dtype=np.complex128).reshape(-1).view(np.float64)
-    o = np.asarray(ref, dtype=np.complex128).reshape(-1).view(np.float64)
+    g = np.ascontiguousarray(got, dtype=np.complex128).reshape(-1).view(np.float64)
+    o = np.ascontiguousarray(ref, dtype=np.complex128).reshape(-1).view(np.float64)
     if g.shape != o.shape:
         raise ValueError(f"shape mismatch {g.shape} vs {o.shape}")
     num = np.longdouble(0)

@@ -1,0 +1,234 @@
+"""paper_0811_2535_b200 -- B200-native MoA reshape-transpose FFT (arXiv 0811.2535).
+
+Thin ctypes binding over ``libmoa_fft.so`` (C ABI in ``include/moa_fft.h``).
+It only marshals arguments: every step of the transform runs in the library's
+CUDA kernels.  There is no CPU path: if the shared library is missing or
+fails to load, importing this package raises.
+
+    import torch, paper_0811_2535_b200 as moa
+    X = moa.fft(x)                       # x: 1-D complex128 CUDA tensor, n = 2^t
+    plan = moa.Plan(n, sign=-1)          # reusable plan
+    plan.execute(x, out)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import build as _build
+
+__all__ = ["Plan", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize",
+           "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "lib_path", "load"]
+
+MODE_LIFTED, MODE_LITERAL, MODE_EMULATED = 0, 1, 2
+_ERRS = {-1: "INVALID_N", -2: "INVALID_P", -3: "INVALID_SIGN", -4: "ALIGN", -5: "NO_DIST",
+         -6: "OOM", -7: "CUDA", -8: "NCCL", -9: "INVALID_ARG"}
+
+
+class MoaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"MOA_ERR_{_ERRS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("nlift", ctypes.c_int), ("lift", ctypes.c_int64 * 4),
+                ("chunks", ctypes.c_int)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("t", ctypes.c_int), ("p", ctypes.c_int), ("rank", ctypes.c_int),
+                ("sign", ctypes.c_int), ("mode", ctypes.c_int), ("local_n", ctypes.c_int64),
+                ("passes", ctypes.c_int), ("lift", ctypes.c_int64 * 4), ("breakpoint", ctypes.c_int),
+                ("chunks", ctypes.c_int), ("launches", ctypes.c_int), ("workspace_bytes", ctypes.c_int64),
+                ("hbm_bytes", ctypes.c_int64), ("a2a_bytes", ctypes.c_int64)]
+
+
+EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host",
+           "moa_fft_destroy", "moa_fft_set_stream", "moa_fft_plan_info", "moa_fft_last_error",
+           "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
+           "moa_fft_version"]
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_needed: bool = True):
+    """Load libmoa_fft.so (building it with nvcc first if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_needed and _build.needs_build():
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"{_build.LIB} is missing; run paper_0811_2535_b200/build.py (no CPU fallback)")
+    lib = ctypes.CDLL(_build.LIB, mode=ctypes.RTLD_GLOBAL)
+    vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    lib.moa_fft_plan.argtypes = [i64, ci, ci]
+    lib.moa_fft_plan.restype = vp
+    lib.moa_fft_plan_ex.argtypes = [i64, ci, ci, ctypes.POINTER(_Options)]
+    lib.moa_fft_plan_ex.restype = vp
+    lib.moa_fft_execute.argtypes = [vp, vp, vp]
+    lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
+    lib.moa_fft_destroy.argtypes = [vp]
+    lib.moa_fft_destroy.restype = None
+    lib.moa_fft_set_stream.argtypes = [vp, vp]
+    lib.moa_fft_plan_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    lib.moa_fft_last_error.restype = ctypes.c_char_p
+    lib.moa_dist_unique_id.argtypes = [vp]
+    lib.moa_dist_init.argtypes = [ci, ci, vp]
+    lib.moa_gen_uniform.argtypes = [ctypes.c_uint64, i64, i64, i64, vp, vp]
+    lib.moa_fft_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _err(code: int):
+    raise MoaError(code, _lib.moa_fft_last_error().decode())
+
+
+def _ptr(x) -> int:
+    return x if isinstance(x, int) else int(x.data_ptr())
+
+
+def _cur_stream() -> int:
+    import torch
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+class Plan:
+    """A reusable transform plan (moa_fft_plan_ex).
+
+    n, p, sign: see include/moa_fft.h.  mode: MODE_LIFTED (product path),
+    MODE_LITERAL (paper-literal bitrev + t radix-2 stages, ablation),
+    MODE_EMULATED (p virtual ranks on one GPU).  lift: optional lifting <F1..Fd>.
+    """
+
+    def __init__(self, n: int, p: int = 1, sign: int = -1, mode: int = MODE_LIFTED,
+                 lift=None, chunks: int = 0, stream=None):
+        lib = load()
+        opt = _Options()
+        opt.mode = mode
+        opt.chunks = chunks
+        if lift:
+            opt.nlift = len(lift)
+            for i, f in enumerate(lift):
+                opt.lift[i] = int(f)
+        h = lib.moa_fft_plan_ex(int(n), int(p), int(sign), ctypes.byref(opt))
+        if not h:
+            raise MoaError(-9, lib.moa_fft_last_error().decode())
+        self._h = h
+        self.n, self.p, self.sign, self.mode = int(n), int(p), int(sign), mode
+        self._stream = None
+        self.set_stream(stream)
+
+    def set_stream(self, stream=None):
+        """Bind to a stream (torch.cuda.Stream, raw handle int, or None = torch's current)."""
+        if stream is None:
+            s = _cur_stream()
+        elif isinstance(stream, int):
+            s = stream
+        else:
+            s = int(stream.cuda_stream)
+        rc = _lib.moa_fft_set_stream(self._h, s)
+        if rc:
+            _err(rc)
+        self._stream = s
+
+    @property
+    def stream(self) -> int:
+        return self._stream
+
+    def info(self) -> dict:
+        inf = _Info()
+        rc = _lib.moa_fft_plan_info(self._h, ctypes.byref(inf))
+        if rc:
+            _err(rc)
+        d = {f: getattr(inf, f) for f, _ in _Info._fields_}
+        d["lift"] = [int(v) for v in inf.lift[: inf.passes]] if self.mode != MODE_LITERAL else []
+        return d
+
+    def execute(self, x, out=None):
+        """Transform device data x (torch complex128 tensor or raw pointer) into out."""
+        if out is None:
+            import torch
+            out = torch.empty_like(x)
+        rc = _lib.moa_fft_execute(self._h, _ptr(x), _ptr(out))
+        if rc:
+            _err(rc)
+        return out
+
+    def execute_host(self, host_in, host_out):
+        """End-to-end: host (ideally pinned) buffers in and out; synchronises."""
+        rc = _lib.moa_fft_execute_host(self._h, _ptr(host_in), _ptr(host_out))
+        if rc:
+            _err(rc)
+        return host_out
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            _lib.moa_fft_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def fft(x, sign: int = -1, out=None):
+    """X_k = sum_j x_j exp(sign 2 pi i jk/n) of a 1-D complex128 CUDA tensor (n = 2^t)."""
+    import torch
+    if x.dtype != torch.complex128 or not x.is_cuda or x.dim() != 1:
+        raise ValueError("fft expects a 1-D complex128 CUDA tensor")
+    x = x.contiguous()
+    plan = Plan(x.numel(), 1, sign)
+    try:
+        return plan.execute(x, out)
+    finally:
+        torch.cuda.current_stream().synchronize()
+        plan.destroy()
+
+
+def ifft_unnormalized(x, out=None):
+    return fft(x, +1, out)
+
+
+def gen_uniform(seed: int, count: int, out, first: int = 0, stride: int = 1, stream=None):
+    """Fill a device buffer with the moa_inputs recipe (x_g = u(2g) + i u(2g+1), g = first + stride*i)."""
+    lib = load()
+    s = _cur_stream() if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
+    rc = lib.moa_gen_uniform(ctypes.c_uint64(seed), int(first), int(stride), int(count), _ptr(out), s)
+    if rc:
+        _err(rc)
+    return out
+
+
+def dist_init(group=None):
+    """Create the library's NCCL communicator over torch.distributed's world (rank 0's id broadcast)."""
+    import torch
+    import torch.distributed as dist
+    lib = load()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = (ctypes.c_char * 128)()
+    if rank == 0:
+        rc = lib.moa_dist_unique_id(buf)
+        if rc:
+            _err(rc)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+    t = torch.frombuffer(bytearray(bytes(buf)), dtype=torch.uint8).to(dev)
+    dist.broadcast(t, 0, group=group)
+    ident = bytes(t.cpu().numpy().tobytes())
+    rc = lib.moa_dist_init(rank, world, ctypes.c_char_p(ident))
+    if rc:
+        _err(rc)
+    return rank, world
+
+
+def dist_finalize():
+    load().moa_dist_finalize()

@@ -1,0 +1,52 @@
+// fft_inst.cu -- instantiates the pass kernel for one FFT length F = 2^MOA_INST_LOGF.
+// Compiled once per length (1..13) with -DMOA_INST_LOGF=<f>, in parallel.
+#include "fft_pass.cuh"
+
+#ifndef MOA_INST_LOGF
+#error "compile with -DMOA_INST_LOGF=<1..13>"
+#endif
+
+#define MOA_CAT2(a, b) a##b
+#define MOA_CAT(a, b) MOA_CAT2(a, b)
+
+namespace moa {
+
+static constexpr int kF = 1 << MOA_INST_LOGF;
+
+template <int T>
+static cudaError_t launch_t(const PassDesc &d, int64_t tiles, cudaStream_t s) {
+    if constexpr (T * kF <= TF_MAX) return launch_one<kF, T>(d, tiles, s);
+    return cudaErrorInvalidValue;
+}
+
+template <int T>
+static cudaError_t prepare_t() {
+    if constexpr (T * kF <= TF_MAX) return prepare_one<kF, T>();
+    return cudaSuccess;
+}
+
+cudaError_t MOA_CAT(launch_pass_f, MOA_INST_LOGF)(int T, const PassDesc &d, int64_t tiles, cudaStream_t s) {
+    switch (T) {
+    case 1: return launch_t<1>(d, tiles, s);
+    case 2: return launch_t<2>(d, tiles, s);
+    case 4: return launch_t<4>(d, tiles, s);
+    case 8: return launch_t<8>(d, tiles, s);
+    case 16: return launch_t<16>(d, tiles, s);
+    case 32: return launch_t<32>(d, tiles, s);
+    case 64: return launch_t<64>(d, tiles, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t MOA_CAT(prepare_pass_f, MOA_INST_LOGF)() {
+    cudaError_t e;
+    if ((e = prepare_t<1>()) != cudaSuccess) return e;
+    if ((e = prepare_t<2>()) != cudaSuccess) return e;
+    if ((e = prepare_t<4>()) != cudaSuccess) return e;
+    if ((e = prepare_t<8>()) != cudaSuccess) return e;
+    if ((e = prepare_t<16>()) != cudaSuccess) return e;
+    if ((e = prepare_t<32>()) != cudaSuccess) return e;
+    return prepare_t<64>();
+}
+
+}  // namespace moa

@@ -1,0 +1,83 @@
+// moa_internal.h -- types shared by the host plan code and the CUDA kernels.
+// Not part of the public ABI (include/moa_fft.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace moa {
+
+constexpr int FMAX_LOG = 13;            // largest on-chip FFT length per pass: 2^13 points
+constexpr int FMAX = 1 << FMAX_LOG;     // (128 KiB of complex128 per CTA)
+constexpr int TF_MAX = 8192;            // T*F <= TF_MAX elements per CTA tile
+
+// One lifted pass: for every tile, T independent F-point
+// DFTs along an axis of stride in_f (the paper's butterfly stages of one
+// lifted level, Fig 3.7 basic block grouped into radix-16 register kernels),
+// an optional twiddle multiply omega_n^(alpha + beta*k) (Fig 4.4's weightcyclic
+// scaling folded into the lifted form), and a store either in place (middle
+// passes) or to the transposed/natural output index K (last pass, the
+// reshape-transpose of P:49-53) or the all-to-all send layout (p > 1, Fig 5.9).
+struct PassDesc {
+    const double2 *src;
+    double2 *dst;
+    const double2 *tw_hi;   // omega_n^(e << hbits) for the two-level table   (sign -1)
+    const double2 *tw_lo;   // omega_n^e, e < 2^hbits                          (sign -1)
+    const double2 *tw_f;    // omega_FMAX^e, e < FMAX: intra-pass stage twiddles (sign -1)
+    // tile id -> (u, v, w):  u = id % U, v = (id / U) % V, w = id / (U * V)
+    int64_t U, V;
+    // input element (tile, t, f): in_u*u + in_v*v + in_w*w + in_t*t + in_f*f
+    int64_t in_u, in_v, in_w, in_t, in_f;
+    // last pass: output index K = K_u*u + K_v*v + K_w*w + K_t*t + K_k*k
+    int64_t K_u, K_v, K_w, K_t, K_k;
+    // twiddle exponent e = alpha + beta*k (mod n),
+    //   alpha = a_u*u + a_v*v + a_w*w + a_t*t,  beta = b_u*u + b_v*v + b_w*w + b_t*t
+    //   (+ the constants a_c, b_c)
+    int64_t a_c, a_u, a_v, a_w, a_t;
+    int64_t b_c, b_u, b_v, b_w, b_t;
+    uint64_t nmask;         // n - 1 (the GLOBAL n of the transform)
+    int hbits;              // split of the two-level table
+    int last;               // 1: store to K (or its pack); 0: store in place at (t, k) of the input view
+    int twiddle;            // 1: multiply by omega_n^e before the store
+    int conj_in, conj_out;  // sign +1 is computed as conj(FFT_-1(conj x))
+    int in_tfast, out_tfast;// lane->(t, j) order of the global-facing stages
+    int pack_lp;            // >= 0: send layout addr = (K & (P-1)) * pack_chunk + (K >> pack_lp)
+    int64_t pack_chunk;
+};
+
+// host-side launchers (kernels.cu / fft_inst.cu)
+int pass_supported(int logF, int T);
+size_t pass_smem_bytes(int logF, int T);
+int pass_threads(int logF, int T);
+cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaStream_t s);
+cudaError_t prepare_pass_kernels();    // raise the dynamic smem limits once
+
+cudaError_t launch_bitrev(const double2 *in, double2 *out, int t, int conj_in, cudaStream_t s);
+cudaError_t launch_radix2_stage(const double2 *in, double2 *out, int t, int q,
+                                const double2 *tw_hi, const double2 *tw_lo, int hbits,
+                                int conj_out, cudaStream_t s);
+cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, int P,
+                            int conj_out, cudaStream_t s);
+cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int64_t count,
+                               double2 *out, cudaStream_t s);
+
+}  // namespace moa
+
+// per-length launchers defined by fft_inst.cu compiled with -DMOA_INST_LOGF=<f>
+#define MOA_DECLARE_INST(f)                                                                 \
+    namespace moa {                                                                         \
+    cudaError_t launch_pass_f##f(int T, const PassDesc &d, int64_t tiles, cudaStream_t s);  \
+    cudaError_t prepare_pass_f##f();                                                        \
+    }
+MOA_DECLARE_INST(1)
+MOA_DECLARE_INST(2)
+MOA_DECLARE_INST(3)
+MOA_DECLARE_INST(4)
+MOA_DECLARE_INST(5)
+MOA_DECLARE_INST(6)
+MOA_DECLARE_INST(7)
+MOA_DECLARE_INST(8)
+MOA_DECLARE_INST(9)
+MOA_DECLARE_INST(10)
+MOA_DECLARE_INST(11)
+MOA_DECLARE_INST(12)
+MOA_DECLARE_INST(13)

@@ -1,0 +1,696 @@
+// plan.cu -- plan builder (dimension lifting + FP64 twiddle tables), executor
+// and the C ABI declared in include/moa_fft.h.
+//
+// Plan = the paper's Phase 3/4 artefacts made concrete for B200:
+//   S0 validation and lifting   n = 2^t, psize = n/p >= p, breakpoint =
+//                               log2(psize)+1 (the high end of §4.8)
+//   S1 twiddle tables           built once per plan in long double (the paper
+//                               recomputes weight(row) every stage)
+//   S3/S4 lifted passes         one PassDesc per level of <F1..Fd>
+//   S5/S6 (p > 1)               the local psize-point FFT whose last pass scales by
+//                               omega_n^(r*k1) and packs for the all-to-all (Fig 5.9)
+//   S7 all-to-all               NCCL grouped send/recv (dist.cu)
+//   S8 cyclic phase             pcombine<P>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/moa_fft.h"
+#include "moa_internal.h"
+
+namespace moa {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(MOA_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+// ------------------------------------------------------------------ NCCL (dist.cu)
+int dist_world(int *rank, int *size);
+int dist_alltoall(const double2 *send, double2 *recv, int64_t chunk, int p, int rank, cudaStream_t s,
+                  std::string *err);
+
+// ------------------------------------------------------------------ twiddles
+// exp(-2 pi i e / N) for N a power of two, evaluated in long double on the
+// first octant of the circle and rounded once to double; quarter turns exact.
+static double2 host_root(uint64_t e, uint64_t N) {
+    e &= N - 1;
+    // position on the circle in units of N/8 (octant) with remainder
+    unsigned __int128 e8 = (unsigned __int128)e * 8;
+    int oct = (int)(e8 / N);
+    uint64_t rem = (uint64_t)(e8 % N);  // angle inside the octant = (pi/4) * rem / N
+    const long double quarter_pi = 0.785398163397448309615660845819875721L;
+    long double a = quarter_pi * ((long double)rem / (long double)N);
+    long double b = quarter_pi - a;  // complementary angle within the octant
+    long double c, s;
+    // cos/sin of theta = oct*pi/4 + a using only angles in [0, pi/4]
+    switch (oct) {
+    case 0: c = cosl(a); s = sinl(a); break;
+    case 1: c = sinl(b); s = cosl(b); break;
+    case 2: c = -sinl(a); s = cosl(a); break;
+    case 3: c = -cosl(b); s = sinl(b); break;
+    case 4: c = -cosl(a); s = -sinl(a); break;
+    case 5: c = -sinl(b); s = -cosl(b); break;
+    case 6: c = sinl(a); s = -cosl(a); break;
+    default: c = cosl(b); s = -sinl(b); break;
+    }
+    return make_double2((double)c, (double)(-s));
+}
+
+// ------------------------------------------------------------------ plan
+struct PassPlan {
+    int logF, T;
+    int64_t tiles;
+    PassDesc d;  // src/dst patched at execute
+};
+
+}  // namespace moa
+
+using namespace moa;
+
+struct moa_fft_plan_s {
+    int64_t n = 0, M = 0;
+    int t = 0, p = 1, rank = 0, sign = -1, mode = MOA_MODE_LIFTED;
+    int d = 0;
+    int64_t lift[4] = {0, 0, 0, 0};
+    int chunks = 1;
+    int device = 0;
+    int hbits = 0;
+    cudaStream_t stream = nullptr;
+    double2 *tw_hi = nullptr, *tw_lo = nullptr, *tw_f = nullptr;
+    double2 *work = nullptr, *send = nullptr, *recv = nullptr;
+    double2 *stage_in = nullptr, *stage_out = nullptr;  // execute_host staging
+    int64_t work_elems = 0, send_elems = 0;
+    std::vector<PassPlan> passes;   // p == 1: all passes; p > 1: phase 1 for rank `rank`
+    std::vector<std::vector<PassPlan>> rank_passes;  // emulated: phase 1 per virtual rank
+    int64_t workspace_bytes = 0;
+    // per-kernel event profiling (moa_fft_set_profiling)
+    bool profiling = false;
+    struct Slot {
+        std::string name;
+        int64_t bytes;
+        int launches;
+        double ms;
+    };
+    struct Rec {
+        int slot;
+        cudaEvent_t a, b;
+    };
+    std::vector<Slot> slots;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+};
+
+namespace moa {
+
+static int ilog2(int64_t v) {
+    int r = 0;
+    while (((int64_t)1 << r) < v) ++r;
+    return r;
+}
+static bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static int env_int(const char *name, int dflt) {
+    const char *s = getenv(name);
+    return (s && *s) ? atoi(s) : dflt;
+}
+
+// default lifting <F1..Fd> of a local length 2^tl (SURVEY §8 notation table)
+static int default_lifting(int tl, int64_t *lift) {
+    if (tl <= FMAX_LOG) {
+        lift[0] = (int64_t)1 << tl;
+        return 1;
+    }
+    if (tl <= 2 * (FMAX_LOG - 1) + 2) {   // two levels up to 2^26
+        int a = tl / 2;
+        lift[0] = (int64_t)1 << a;
+        lift[1] = (int64_t)1 << (tl - a);
+        return 2;
+    }
+    if (tl <= 3 * FMAX_LOG) {
+        int a = tl / 3, b = (tl - a) / 2;
+        lift[0] = (int64_t)1 << a;
+        lift[1] = (int64_t)1 << b;
+        lift[2] = (int64_t)1 << (tl - a - b);
+        return 3;
+    }
+    int a = tl / 4, b = (tl - a) / 3, c = (tl - a - b) / 2;
+    lift[0] = (int64_t)1 << a;
+    lift[1] = (int64_t)1 << b;
+    lift[2] = (int64_t)1 << c;
+    lift[3] = (int64_t)1 << (tl - a - b - c);
+    return 4;
+}
+
+static int choose_T(int logF, int64_t avail) {
+    int tf_max = env_int("MOA_FFT_TF", TF_MAX);
+    if (tf_max > TF_MAX) tf_max = TF_MAX;
+    int T = 1;
+    while (T < 64 && ((int64_t)(2 * T) << logF) <= tf_max && 2 * T <= avail) T *= 2;
+    while (T > 1 && !pass_supported(logF, T)) T /= 2;
+    return T;
+}
+
+// Build the passes of a local FFT of length M = prod(lift) (global length n).
+// rank >= 0 with P > 1: the last pass scales by omega_n^(rank*K) and packs to
+// the send layout [dst][c] with K = dst + P*c (S6, fused into S4's epilogue).
+static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan> &out) {
+    const int d = pl->d;
+    const int64_t *Fv = pl->lift;
+    const int64_t n = pl->n;
+    out.clear();
+    for (int i = 0; i < d; ++i) {
+        PassPlan pp;
+        memset(&pp.d, 0, sizeof(PassDesc));
+        PassDesc &D = pp.d;
+        const int64_t F = Fv[i];
+        int64_t A = 1, B = 1;
+        for (int l = 0; l < i; ++l) A *= Fv[l];
+        for (int l = i + 1; l < d; ++l) B *= Fv[l];
+        pp.logF = ilog2(F);
+        D.nmask = (uint64_t)n - 1;
+        D.hbits = pl->hbits;
+        D.tw_hi = pl->tw_hi;
+        D.tw_lo = pl->tw_lo;
+        D.tw_f = pl->tw_f;
+        D.pack_lp = -1;
+        D.conj_in = (i == 0 && pl->sign > 0);
+        D.conj_out = 0;
+        if (i < d - 1) {
+            // middle pass: view [A][F][B], F-point DFTs along the middle axis for
+            // every (a, b); twiddle omega_{F*B}^(b*k) = omega_n^(b*k*n/(F*B)); in place.
+            int T = choose_T(pp.logF, B);
+            pp.T = T;
+            D.U = B / T;
+            D.V = A;
+            D.in_u = T;
+            D.in_v = F * B;
+            D.in_t = 1;
+            D.in_f = B;
+            int64_t mult = n / (F * B);
+            D.twiddle = 1;
+            D.b_u = mult * T;
+            D.b_t = mult;
+            D.in_tfast = T > 1;
+            D.out_tfast = T > 1;
+            D.last = 0;
+            pp.tiles = D.U * D.V;
+        } else {
+            // last pass: rows of length F indexed by the digits (k_0 .. k_{d-2}) the
+            // earlier passes produced (k_0 most significant); output index
+            // K = k_0 + F_0 k_1 + F_0 F_1 k_2 + ... + (F_0..F_{d-2}) k : the
+            // transpose <d-1 .. 0> + ravel of Fig A.1, i.e. natural order.
+            D.last = 1;
+            D.in_f = 1;
+            D.in_tfast = 0;
+            int64_t S[3] = {0, 0, 0};   // stride (in rows) of digit k_l in the row index
+            for (int l = 0; l < d - 1; ++l) {
+                int64_t s = 1;
+                for (int m = l + 1; m < d - 1; ++m) s *= Fv[m];
+                S[l] = s;
+            }
+            int64_t Kk = A;
+            int64_t K_d1 = d >= 3 ? Fv[0] : 0;      // weight of k_1
+            int64_t K_d2 = d >= 4 ? Fv[0] * Fv[1] : 0;
+            if (d == 1) {
+                pp.T = 1;
+                D.U = 1;
+                D.V = 1;
+                D.K_k = 1;
+                D.out_tfast = 0;
+                pp.tiles = 1;
+                if (P > 1) {
+                    D.pack_lp = ilog2(P);
+                    D.pack_chunk = pl->M / P;
+                }
+            } else if (P > 1) {
+                if (d > 3) return fail(MOA_ERR_INVALID_ARG, "p > 1 supports lifting depth <= 3");
+                // rows k_0 = dst + P*(cb*T + t): every row of a tile goes to one destination
+                int T = choose_T(pp.logF, Fv[0] / P);
+                pp.T = T;
+                D.U = Fv[0] / (P * T);
+                D.V = P;
+                D.in_u = P * T * S[0] * F;
+                D.in_v = S[0] * F;
+                D.in_t = P * S[0] * F;
+                D.in_w = d >= 3 ? S[1] * F : 0;
+                D.K_u = P * T;
+                D.K_v = 1;
+                D.K_t = P;
+                D.K_w = K_d1;
+                D.K_k = Kk;
+                D.out_tfast = T > 1;
+                D.pack_lp = ilog2(P);
+                D.pack_chunk = pl->M / P;
+                pp.tiles = D.U * D.V * (d >= 3 ? Fv[1] : 1);
+            } else {
+                int T = choose_T(pp.logF, Fv[0]);
+                pp.T = T;
+                D.U = Fv[0] / T;
+                D.V = d >= 3 ? Fv[1] : 1;
+                D.in_u = T * S[0] * F;
+                D.in_t = S[0] * F;
+                D.in_v = d >= 3 ? S[1] * F : 0;
+                D.in_w = d >= 4 ? S[2] * F : 0;
+                D.K_u = T;
+                D.K_t = 1;
+                D.K_v = K_d1;
+                D.K_w = K_d2;
+                D.K_k = Kk;
+                D.out_tfast = T > 1;
+                pp.tiles = D.U * D.V * (d >= 4 ? Fv[2] : 1);
+            }
+            if (P > 1 && rank > 0) {
+                // S6: Y_r[K] <- omega_n^(r*K) Y_r[K]  (weightcyclic, Fig 4.4)
+                uint64_t r = (uint64_t)rank;
+                D.twiddle = 1;
+                D.a_u = (int64_t)(r * (uint64_t)D.K_u);
+                D.a_v = (int64_t)(r * (uint64_t)D.K_v);
+                D.a_w = (int64_t)(r * (uint64_t)D.K_w);
+                D.a_t = (int64_t)(r * (uint64_t)D.K_t);
+                D.b_c = (int64_t)(r * (uint64_t)D.K_k);
+            }
+            D.conj_out = (P == 1 && pl->sign > 0);
+        }
+        if (!pass_supported(pp.logF, pp.T))
+            return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
+        out.push_back(pp);
+    }
+    return MOA_OK;
+}
+
+static void free_plan(moa_fft_plan_s *pl) {
+    if (!pl) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->device);
+    cudaStreamSynchronize(pl->stream);
+    cudaFree(pl->tw_hi);
+    cudaFree(pl->tw_lo);
+    cudaFree(pl->tw_f);
+    cudaFree(pl->work);
+    cudaFree(pl->send);
+    cudaFree(pl->recv);
+    cudaFree(pl->stage_in);
+    cudaFree(pl->stage_out);
+    for (auto &r : pl->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : pl->pool) cudaEventDestroy(e);
+    cudaSetDevice(cur);
+    delete pl;
+}
+
+static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_plan_s **res) {
+    *res = nullptr;
+    int mode = opt ? opt->mode : MOA_MODE_LIFTED;
+    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 34))
+        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 34 (Fig 2.1: n = 2^t, t >= 1)",
+                    (long long)n);
+    if (sign != -1 && sign != 1) return fail(MOA_ERR_INVALID_SIGN, "sign=%d must be -1 or +1", sign);
+    if (mode < MOA_MODE_LIFTED || mode > MOA_MODE_EMULATED)
+        return fail(MOA_ERR_INVALID_ARG, "unknown mode %d", mode);
+    if (!pow2(p) || p > 16) return fail(MOA_ERR_INVALID_P, "p=%d must be a power of two <= 16", p);
+    if (n / p < p)
+        return fail(MOA_ERR_INVALID_P, "psize = n/p = %lld < p = %d violates psize >= m (P:289)",
+                    (long long)(n / p), p);
+    if (mode == MOA_MODE_LITERAL && p != 1)
+        return fail(MOA_ERR_INVALID_P, "literal mode is single-GPU (p must be 1, got %d)", p);
+    if (mode == MOA_MODE_EMULATED && p < 2) return fail(MOA_ERR_INVALID_P, "emulated mode needs p >= 2");
+    int rank = 0;
+    if (p > 1 && mode != MOA_MODE_EMULATED) {
+        int wr = -1, ws = 0;
+        if (dist_world(&wr, &ws) != MOA_OK || ws == 0)
+            return fail(MOA_ERR_NO_DIST, "p=%d > 1 needs moa_dist_init first", p);
+        if (ws != p) return fail(MOA_ERR_INVALID_P, "p=%d differs from the world size %d", p, ws);
+        rank = wr;
+    }
+    moa_fft_plan_s *pl = new moa_fft_plan_s();
+    pl->n = n;
+    pl->t = ilog2(n);
+    pl->p = p;
+    pl->rank = rank;
+    pl->sign = sign;
+    pl->mode = mode;
+    pl->M = n / p;
+    CUDA_TRY(cudaGetDevice(&pl->device));
+    int tl = ilog2(pl->M);
+    if (opt && opt->nlift > 0) {
+        if (opt->nlift > 4) {
+            delete pl;
+            return fail(MOA_ERR_INVALID_ARG, "lifting depth %d > 4", opt->nlift);
+        }
+        int64_t prod = 1;
+        for (int i = 0; i < opt->nlift; ++i) {
+            int64_t F = opt->lift[i];
+            if (!pow2(F) || F < 2 || F > FMAX) {
+                delete pl;
+                return fail(MOA_ERR_INVALID_ARG, "lifting factor %lld outside powers of two in [2, %d]",
+                            (long long)F, FMAX);
+            }
+            pl->lift[i] = F;
+            prod *= F;
+        }
+        if (prod != pl->M) {
+            delete pl;
+            return fail(MOA_ERR_INVALID_ARG, "lifting product %lld != local length %lld", (long long)prod,
+                        (long long)pl->M);
+        }
+        pl->d = opt->nlift;
+    } else {
+        pl->d = default_lifting(tl, pl->lift);
+    }
+    if (p > 1 && pl->lift[0] < p && pl->d > 1) {
+        delete pl;
+        return fail(MOA_ERR_INVALID_ARG, "first lifting factor %lld < p=%d", (long long)pl->lift[0], p);
+    }
+    pl->chunks = 1;
+
+    // ---- S1: twiddle tables (sign -1; sign +1 runs conj(FFT(conj x)))
+    pl->hbits = (pl->t + 1) / 2;
+    int64_t nlo = (int64_t)1 << pl->hbits, nhi = (int64_t)1 << (pl->t - pl->hbits);
+    std::vector<double2> hlo(nlo), hhi(nhi), hf(FMAX);
+    for (int64_t e = 0; e < nlo; ++e) hlo[e] = host_root((uint64_t)e, (uint64_t)n);
+    for (int64_t e = 0; e < nhi; ++e) hhi[e] = host_root((uint64_t)e << pl->hbits, (uint64_t)n);
+    for (int e = 0; e < FMAX; ++e) hf[e] = host_root((uint64_t)e, FMAX);
+    int rc = MOA_OK;
+    auto alloc = [&](double2 **ptr, int64_t elems) -> int {
+        if (elems <= 0) return MOA_OK;
+        cudaError_t e = cudaMalloc((void **)ptr, (size_t)elems * sizeof(double2));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MOA_ERR_OOM, "cudaMalloc(%lld bytes) failed: %s", (long long)(elems * 16),
+                        cudaGetErrorString(e));
+        }
+        pl->workspace_bytes += elems * (int64_t)sizeof(double2);
+        return MOA_OK;
+    };
+    if ((rc = alloc(&pl->tw_lo, nlo)) || (rc = alloc(&pl->tw_hi, nhi)) || (rc = alloc(&pl->tw_f, FMAX))) {
+        free_plan(pl);
+        return rc;
+    }
+    cudaError_t ce;
+    if ((ce = cudaMemcpy(pl->tw_lo, hlo.data(), nlo * 16, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (ce = cudaMemcpy(pl->tw_hi, hhi.data(), nhi * 16, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (ce = cudaMemcpy(pl->tw_f, hf.data(), FMAX * 16, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        free_plan(pl);
+        return fail(MOA_ERR_CUDA, "twiddle upload failed: %s", cudaGetErrorString(ce));
+    }
+    static bool prepared = false;
+    if (!prepared) {
+        if ((ce = prepare_pass_kernels()) != cudaSuccess) {
+            free_plan(pl);
+            return fail(MOA_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(ce));
+        }
+        prepared = true;
+    }
+
+    // ---- buffers and passes
+    if (mode == MOA_MODE_LITERAL) {
+        pl->work_elems = n;
+    } else {
+        pl->work_elems = pl->d > 1 ? pl->M : 0;
+        if (p > 1) pl->send_elems = (mode == MOA_MODE_EMULATED) ? n : pl->M;
+    }
+    if ((rc = alloc(&pl->work, pl->work_elems)) || (rc = alloc(&pl->send, pl->send_elems)) ||
+        (rc = alloc(&pl->recv, pl->send_elems))) {
+        free_plan(pl);
+        return rc;
+    }
+    if (mode == MOA_MODE_EMULATED) {
+        pl->rank_passes.resize(p);
+        for (int r = 0; r < p; ++r)
+            if ((rc = build_passes(pl, r, p, pl->rank_passes[r])) != MOA_OK) {
+                free_plan(pl);
+                return rc;
+            }
+    } else if (mode == MOA_MODE_LIFTED) {
+        if ((rc = build_passes(pl, rank, p, pl->passes)) != MOA_OK) {
+            free_plan(pl);
+            return rc;
+        }
+    }
+    *res = pl;
+    return MOA_OK;
+}
+
+static bool aligned16(const void *ptr) { return ptr && ((uintptr_t)ptr & 15) == 0; }
+
+// ---- event profiling: a scope records an event pair around one launch
+static cudaEvent_t pool_event(moa_fft_plan_s *pl) {
+    if (!pl->pool.empty()) {
+        cudaEvent_t e = pl->pool.back();
+        pl->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    moa_fft_plan_s *pl;
+    int slot = -1;
+    cudaEvent_t a = nullptr;
+    ProfScope(moa_fft_plan_s *p, const std::string &name, int64_t bytes) : pl(p) {
+        if (!pl->profiling) return;
+        for (size_t i = 0; i < pl->slots.size(); ++i)
+            if (pl->slots[i].name == name) slot = (int)i;
+        if (slot < 0) {
+            pl->slots.push_back({name, bytes, 0, 0.0});
+            slot = (int)pl->slots.size() - 1;
+        }
+        a = pool_event(pl);
+        cudaEventRecord(a, pl->stream);
+    }
+    ~ProfScope() {
+        if (!pl->profiling || !a) return;
+        cudaEvent_t b = pool_event(pl);
+        cudaEventRecord(b, pl->stream);
+        pl->recs.push_back({slot, a, b});
+    }
+};
+
+// run the lifted passes of one (virtual) rank: in -> [work] -> out
+static int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in, double2 *out) {
+    const int d = (int)ps.size();
+    for (int i = 0; i < d; ++i) {
+        PassDesc D = ps[i].d;
+        D.src = (i == 0) ? in : pl->work;
+        D.dst = (i == d - 1) ? out : pl->work;
+        char name[64];
+        snprintf(name, sizeof name, "pass%d fft_pass<F=%d,T=%d>", i, 1 << ps[i].logF, ps[i].T);
+        ProfScope ps_(pl, name, 32 * pl->M);
+        cudaError_t e = launch_pass(ps[i].logF, ps[i].T, D, ps[i].tiles, pl->stream);
+        if (e != cudaSuccess)
+            return fail(MOA_ERR_CUDA, "pass %d (F=2^%d, T=%d) launch failed: %s", i, ps[i].logF, ps[i].T,
+                        cudaGetErrorString(e));
+    }
+    return MOA_OK;
+}
+
+static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
+    cudaStream_t s = pl->stream;
+    if (pl->mode == MOA_MODE_LITERAL) {
+        // Fig 2.1 literally: (1) x <- P_n x; (2)-(7) t radix-2 stages (Fig 3.9)
+        const int t = pl->t;
+        {
+            ProfScope sc(pl, "bitrev", 32 * pl->n);
+            CUDA_TRY(launch_bitrev(in, pl->work, t, pl->sign > 0, s));
+        }
+        for (int q = 1; q <= t; ++q) {
+            const double2 *src = (q == 1) ? pl->work : out;
+            ProfScope sc(pl, "radix2_stage", 32 * pl->n);
+            CUDA_TRY(launch_radix2_stage(src, out, t, q, pl->tw_hi, pl->tw_lo, pl->hbits,
+                                         (q == t) && pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
+    if (pl->p == 1) return run_passes(pl, pl->passes, in, out);
+
+    const int P = pl->p;
+    const int64_t M = pl->M, chunk = M / P;
+    if (pl->mode == MOA_MODE_EMULATED) {
+        for (int r = 0; r < P; ++r) {
+            int rc = run_passes(pl, pl->rank_passes[r], in + r * M, pl->send + r * M);
+            if (rc) return rc;
+        }
+        // S7 emulated: recv_d[s] = send_s[d]  (Fig 5.9 SEND/RECEIVE)
+        for (int dd = 0; dd < P; ++dd)
+            for (int sr = 0; sr < P; ++sr)
+                CUDA_TRY(cudaMemcpyAsync(pl->recv + dd * M + sr * chunk, pl->send + sr * M + dd * chunk,
+                                         chunk * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        for (int dd = 0; dd < P; ++dd) {
+            ProfScope sc(pl, "pcombine", 32 * M);
+            CUDA_TRY(launch_pcombine(pl->recv + dd * M, out + dd * M, chunk, P, pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
+    int rc = run_passes(pl, pl->passes, in, pl->send);
+    if (rc) return rc;
+    std::string err;
+    {
+        ProfScope sc(pl, "alltoall (NCCL)", 16 * chunk * (P - 1));
+        rc = dist_alltoall(pl->send, pl->recv, chunk, P, pl->rank, s, &err);
+    }
+    if (rc) return fail(rc, "%s", err.c_str());
+    ProfScope sc(pl, "pcombine", 32 * M);
+    CUDA_TRY(launch_pcombine(pl->recv, out, chunk, P, pl->sign > 0, s));
+    return MOA_OK;
+}
+
+}  // namespace moa
+
+// ====================================================================== C ABI
+extern "C" {
+
+moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options *opts) {
+    g_err.clear();
+    moa_fft_plan_s *pl = nullptr;
+    if (make_plan(n, p, sign, opts, &pl) != MOA_OK) return nullptr;
+    return pl;
+}
+
+moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign) { return moa_fft_plan_ex(n, p, sign, nullptr); }
+
+int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    if (!aligned16(in) || !aligned16(out))
+        return fail(MOA_ERR_ALIGN, "in/out must be non-NULL 16-byte aligned device pointers");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != pl->device) cudaSetDevice(pl->device);
+    int rc = execute(pl, (const double2 *)in, (double2 *)out);
+    if (cur != pl->device) cudaSetDevice(cur);
+    return rc;
+}
+
+int moa_fft_execute_host(moa_fft_plan_t pl, const void *host_in, void *host_out) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    if (!host_in || !host_out) return fail(MOA_ERR_ALIGN, "NULL host buffer");
+    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M;
+    size_t bytes = (size_t)elems * sizeof(double2);
+    if (!pl->stage_in) {
+        if (cudaMalloc((void **)&pl->stage_in, bytes) != cudaSuccess ||
+            cudaMalloc((void **)&pl->stage_out, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MOA_ERR_OOM, "staging allocation of 2 x %zu bytes failed", bytes);
+        }
+        pl->workspace_bytes += 2 * (int64_t)bytes;
+    }
+    CUDA_TRY(cudaMemcpyAsync(pl->stage_in, host_in, bytes, cudaMemcpyHostToDevice, pl->stream));
+    int rc = moa_fft_execute(pl, pl->stage_in, pl->stage_out);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(host_out, pl->stage_out, bytes, cudaMemcpyDeviceToHost, pl->stream));
+    CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    return MOA_OK;
+}
+
+void moa_fft_destroy(moa_fft_plan_t pl) { free_plan(pl); }
+
+int moa_fft_set_stream(moa_fft_plan_t pl, void *stream) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    pl->stream = (cudaStream_t)stream;
+    return MOA_OK;
+}
+
+int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
+    if (!pl || !o) return fail(MOA_ERR_INVALID_ARG, "NULL plan or info");
+    memset(o, 0, sizeof *o);
+    o->n = pl->n;
+    o->t = pl->t;
+    o->p = pl->p;
+    o->rank = pl->rank;
+    o->sign = pl->sign;
+    o->mode = pl->mode;
+    o->local_n = pl->M;
+    o->passes = pl->mode == MOA_MODE_LITERAL ? pl->t + 1 : pl->d;
+    for (int i = 0; i < 4; ++i) o->lift[i] = pl->lift[i];
+    o->breakpoint = ilog2(pl->M) + 1;
+    o->chunks = pl->chunks;
+    if (pl->mode == MOA_MODE_LITERAL) {
+        o->launches = pl->t + 1;
+        o->hbm_bytes = 32 * pl->n * (pl->t + 1);
+    } else if (pl->p == 1) {
+        o->launches = pl->d;
+        o->hbm_bytes = 32 * pl->n * pl->d;
+    } else {
+        int per_rank = pl->d + 1;
+        o->launches = pl->mode == MOA_MODE_EMULATED ? pl->p * per_rank : per_rank;
+        o->hbm_bytes = 32 * pl->M * (pl->d + 1) * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
+        o->a2a_bytes = 16 * pl->M / pl->p * (pl->p - 1) * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
+    }
+    o->workspace_bytes = pl->workspace_bytes;
+    return MOA_OK;
+}
+
+const char *moa_fft_last_error(void) { return g_err.c_str(); }
+
+int moa_fft_set_profiling(moa_fft_plan_t pl, int enable) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    pl->profiling = enable != 0;
+    return MOA_OK;
+}
+
+int moa_fft_get_profile(moa_fft_plan_t pl, moa_fft_kernel_stat *stats, int max_stats) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    for (auto &sl : pl->slots) {
+        sl.launches = 0;
+        sl.ms = 0;
+    }
+    for (auto &r : pl->recs) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+        pl->slots[r.slot].launches += 1;
+        pl->slots[r.slot].ms += ms;
+        pl->pool.push_back(r.a);
+        pl->pool.push_back(r.b);
+    }
+    pl->recs.clear();
+    int k = 0;
+    for (auto &sl : pl->slots) {
+        if (k >= max_stats || !stats) break;
+        memset(&stats[k], 0, sizeof stats[k]);
+        snprintf(stats[k].name, sizeof stats[k].name, "%s", sl.name.c_str());
+        stats[k].launches = sl.launches;
+        stats[k].total_ms = sl.ms;
+        stats[k].alg_bytes = sl.bytes;
+        ++k;
+    }
+    return k;
+}
+
+int moa_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int64_t count, void *out, void *stream) {
+    if (count < 0) return fail(MOA_ERR_INVALID_ARG, "negative count");
+    if (count > 0 && !aligned16(out)) return fail(MOA_ERR_ALIGN, "out must be a 16-byte aligned device pointer");
+    CUDA_TRY(launch_gen_uniform(seed, first, stride, count, (double2 *)out, (cudaStream_t)stream));
+    return MOA_OK;
+}
+
+const char *moa_fft_version(void) { return "moa-fft-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

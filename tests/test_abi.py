@@ -1,0 +1,80 @@
+"""CPU-side checks of the C-ABI boundary: the library builds, loads, exports
+every symbol include/moa_fft.h declares, and validates its arguments (naming
+the violated bound) before it touches a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_0811_2535_b200 as moa
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = []
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if not fn.endswith(".h"):
+            continue
+        src = open(os.path.join(ROOT, "include", fn)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"\b(moa_[a-z0-9_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = _declared_functions()
+    for required in ("moa_fft_plan", "moa_fft_execute", "moa_fft_destroy", "moa_fft_set_stream",
+                     "moa_dist_init", "moa_dist_finalize", "moa_fft_plan_info", "moa_fft_last_error"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = moa.load()
+    missing = [n for n in _declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(moa.EXPORTS) <= set(_declared_functions())
+    assert b"sm_100a" in lib.moa_fft_version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", moa.lib_path()], capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("n,p,sign,code,needle", [
+    (6, 1, -1, -1, "2^t"),
+    (1, 1, -1, -1, "2^t"),
+    (0, 1, -1, -1, "2^t"),
+    (1 << 35, 1, -1, -1, "t <= 34"),
+    (16, 1, 0, -3, "sign"),
+    (16, 3, -1, -2, "power of two"),
+    (16, 8, -1, -2, "psize >= m"),     # n=16, m=8 rejected
+])
+def test_plan_validation_errors(n, p, sign, code, needle):
+    lib = moa.load()
+    h = lib.moa_fft_plan(n, p, sign)
+    assert not h
+    msg = lib.moa_fft_last_error().decode()
+    assert needle in msg, msg
+    with pytest.raises(moa.MoaError) as e:
+        moa.Plan(n, p, sign)
+    assert e.value.code == -9  # Plan() wraps NULL as INVALID_ARG but keeps the message
+    assert needle in str(e.value)
+
+
+def test_execute_rejects_null_plan():
+    lib = moa.load()
+    assert lib.moa_fft_execute(None, None, None) == -9
+    assert lib.moa_fft_plan_info(None, None) == -9
+    lib.moa_fft_destroy(None)  # NULL-safe
+
+
+def test_dist_plan_without_init_is_rejected():
+    lib = moa.load()
+    h = lib.moa_fft_plan(1 << 10, 2, -1)
+    assert not h
+    assert "moa_dist_init" in lib.moa_fft_last_error().decode()

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): relative L2 error <= 1e-12 * log2(n) in
+complex128, element by element on the same seeded inputs (moa_inputs).  The
+oracle is Fig 3.9 (oracle.fft) and, where n is too large for it, the plain
+definition at sampled bins (oracle.dft_bins).
+"""
+import numpy as np
+import pytest
+
+import moa_inputs
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_0811_2535_b200 as moa  # noqa: E402
+
+
+def tol(t):
+    return 1e-12 * t
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+
+
+def _run(plan, x_np, inplace=False):
+    x = _dev(x_np)
+    if inplace:
+        plan.execute(x, x)
+        out = x
+    else:
+        out = plan.execute(x)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    moa.load()
+
+
+# ------------------------------------------------------------------ generator twin
+def test_gen_uniform_bit_exact():
+    for t, first, stride, count in [(10, 0, 1, 1024), (16, 3, 8, 8191), (20, 0, 1, 1 << 20)]:
+        out = torch.empty(count, dtype=torch.complex128, device="cuda")
+        moa.gen_uniform(moa_inputs.seed_for(t), count, out, first=first, stride=stride)
+        want = moa_inputs.complex_signal(moa_inputs.seed_for(t), count, first=first, stride=stride)
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
+# ------------------------------------------------------------------ single GPU, lifted (product)
+@pytest.mark.parametrize("t", list(range(1, 23)))
+def test_lifted_all_sizes_both_signs(t):
+    x = moa_inputs.signal_for(t)
+    for sign in (-1, 1):
+        ref = oracle.fft(x, sign, threads=8)
+        plan = moa.Plan(1 << t, 1, sign)
+        got = _run(plan, x)
+        err = oracle.rel_l2(got, ref)
+        assert err <= tol(t), (t, sign, err, plan.info())
+
+
+@pytest.mark.parametrize("t,lift", [
+    (12, [64, 64]), (12, [16, 256]), (12, [4096]), (13, [8192]), (14, [2, 8192]),
+    (16, [256, 256]), (16, [16, 16, 256]), (18, [8, 32, 1024]), (20, [1024, 1024]),
+    (20, [4096, 256]), (20, [128, 8192]), (20, [64, 128, 128]), (20, [16, 16, 16, 256]),
+    (21, [8192, 256]), (22, [2048, 2048]),
+])
+def test_lifted_explicit_liftings(t, lift):
+    x = moa_inputs.signal_for(t)
+    ref = oracle.fft(x, -1, threads=8)
+    got = _run(moa.Plan(1 << t, 1, -1, lift=lift), x)
+    assert oracle.rel_l2(got, ref) <= tol(t), lift
+
+
+@pytest.mark.parametrize("t", [3, 10, 14, 20])
+def test_inplace_equals_out_of_place_bitwise(t):
+    x = moa_inputs.signal_for(t)
+    plan = moa.Plan(1 << t)
+    a = _run(plan, x)
+    b = _run(plan, x, inplace=True)
+    c = _run(plan, x)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_input_not_modified():
+    x = moa_inputs.signal_for(16)
+    xd = _dev(x)
+    moa.Plan(1 << 16).execute(xd)
+    torch.cuda.synchronize()
+    assert np.array_equal(xd.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("t", [10, 20])
+def test_round_trip(t):
+    x = moa_inputs.signal_for(t)
+    X = moa.fft(_dev(x), -1)
+    back = moa.fft(X, +1) / (1 << t)
+    assert oracle.rel_l2(back.cpu().numpy(), x) <= tol(t)
+
+
+def test_impulse_and_tone():
+    t = 16
+    n = 1 << t
+    x = np.zeros(n, complex)
+    x[0] = 1
+    got = _run(moa.Plan(n), x)
+    assert np.max(np.abs(got - 1)) <= 1e-14
+    j = np.arange(n)
+    x = np.exp(2j * np.pi * 5 * j / n)
+    got = _run(moa.Plan(n), x)
+    want = np.zeros(n, complex)
+    want[5] = n
+    assert np.max(np.abs(got - want)) / n <= 1e-13
+
+
+def test_against_cufft_cross_check():
+    # independent library cross-check (tests only): torch.fft uses cuFFT
+    t = 20
+    x = _dev(moa_inputs.signal_for(t))
+    ours = moa.fft(x)
+    ref = torch.fft.fft(x)
+    assert oracle.rel_l2(ours.cpu().numpy(), ref.cpu().numpy()) <= tol(t)
+
+
+def test_execute_host_end_to_end():
+    t = 18
+    x = moa_inputs.signal_for(t)
+    hin = torch.from_numpy(x).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    plan = moa.Plan(1 << t)
+    plan.execute_host(hin, hout)
+    assert oracle.rel_l2(hout.numpy(), oracle.fft(x, -1, threads=8)) <= tol(t)
+
+
+def test_plan_info():
+    info = moa.Plan(1 << 24).info()
+    assert info["passes"] == 2 and info["lift"] == [4096, 4096]
+    assert info["hbm_bytes"] == 32 * (1 << 24) * 2
+    assert info["breakpoint"] == 25
+    info = moa.Plan(1 << 30 if False else 1 << 27).info()
+    assert info["passes"] == 3
+
+
+def test_misaligned_pointer_rejected():
+    x = torch.zeros(1 << 10 + 1, dtype=torch.complex128, device="cuda")
+    plan = moa.Plan(1 << 10)
+    with pytest.raises(moa.MoaError):
+        plan.execute(x.data_ptr() + 8, x.data_ptr() + 8)
+
+
+# ------------------------------------------------------------------ paper-literal mode (ablation)
+@pytest.mark.parametrize("t", [1, 2, 5, 9, 10, 11, 16, 20])
+def test_literal_mode(t):
+    x = moa_inputs.signal_for(t)
+    for sign in (-1, 1):
+        got = _run(moa.Plan(1 << t, 1, sign, mode=moa.MODE_LITERAL), x)
+        assert oracle.rel_l2(got, oracle.fft(x, sign, threads=8)) <= tol(t)
+
+
+# ------------------------------------------------------------------ p virtual ranks on one GPU
+@pytest.mark.parametrize("t,P", [(2, 2), (4, 2), (6, 8), (10, 2), (10, 4), (10, 8), (14, 4), (20, 2),
+                                 (20, 4), (20, 8), (22, 8)])
+def test_emulated_distributed(t, P):
+    """rank r holds x[r + P j] and ends with X[r + P i] (xcyclic)."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    for sign in (-1, 1):
+        ref = oracle.fft(x, sign, threads=8)
+        got = _run(moa.Plan(n, P, sign, mode=moa.MODE_EMULATED), xin).reshape(P, n // P)
+        num = den = 0
+        for r in range(P):
+            a, b = oracle.l2_parts(got[r], ref[r::P])
+            num += a
+            den += b
+        assert float(np.sqrt(num / den)) <= tol(t), (t, P, sign)
+
+
+def test_emulated_with_lifting_depth3():
+    t, P = 21, 4
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    ref = oracle.fft(x, -1, threads=8)
+    got = _run(moa.Plan(1 << t, P, -1, mode=moa.MODE_EMULATED, lift=[32, 128, 128]), xin)
+    got = got.reshape(P, -1)
+    assert max(oracle.rel_l2(got[r], ref[r::P]) for r in range(P)) <= tol(t)
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_config_2_24_full_parity():
+    t = 24
+    x = moa_inputs.signal_for(t)
+    got = _run(moa.Plan(1 << t), x)
+    ref = oracle.fft(x, -1, threads=8)
+    assert oracle.rel_l2(got, ref) <= tol(t)
+
+
+@pytest.mark.slow
+def test_config_2_30_sampled_bins():
+    """n = 2^30 (16 GiB), the launch configuration bench.py would use, checked on
+    sampled bins against the plain definition plus Parseval on the whole output."""
+    t = 30
+    n = 1 << t
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(moa_inputs.seed_for(t), n, x)
+    out = moa.Plan(n).execute(x)
+    torch.cuda.synchronize()
+    ks = np.array([0, 1, 12345, n // 2, n - 1])
+    got = out[torch.from_numpy(ks).cuda()].cpu().numpy()
+    xh = x.cpu().numpy()
+    ref = oracle.dft_bins(xh, ks)
+    assert oracle.rel_l2(got, ref) <= tol(t)
+    lhs = torch.sum(out.abs() ** 2).item()
+    rhs = n * torch.sum(x.abs() ** 2).item()
+    assert abs(lhs - rhs) / rhs <= 1e-12

@@ -127,6 +127,17 @@ def test_fft_equals_bruteforce_dft(t):
         assert oracle.rel_l2(oracle.fft(x, sign), oracle.dft(x, sign)) <= 1e-14
 
 
+def test_dft_bins_equals_definition():
+    for t in (1, 5, 10):
+        x = moa_inputs.signal_for(t)
+        ks = np.arange(1 << t)
+        for sign in SIGNS:
+            assert oracle.rel_l2(oracle.dft_bins(x, ks, sign), oracle.dft(x, sign)) <= 1e-15
+    x = moa_inputs.signal_for(16)
+    ks = [0, 1, 777, 40000, 65535]
+    assert oracle.rel_l2(oracle.dft_bins(x, ks), np.fft.fft(x)[ks]) <= 1e-14
+
+
 def test_dft_non_power_of_two_against_numpy():
     # the definition itself, for lengths the FFT cannot take
     for n in (1, 3, 5, 6, 7, 12, 31):
