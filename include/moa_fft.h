@@ -144,6 +144,24 @@ typedef struct {
 int moa_fft_set_profiling(moa_fft_plan_t plan, int enable);
 int moa_fft_get_profile(moa_fft_plan_t plan, moa_fft_kernel_stat *stats, int max_stats);
 
+/*
+ * Host-only introspection of the plan builder (no GPU needed): the index maps
+ * pass `pass` of the lifted local transform uses on rank `rank` of p.
+ * For every element the pass touches, enumerated tile by tile, row t by row,
+ * point f (so consecutive groups of `F` entries are one F-point transform,
+ * F = lifting factor of that pass):
+ *   in_idx[i]  = local input index read for point f,
+ *   out_idx[i] = index written for output k = f (local work index for middle
+ *                passes, natural local output index for the last pass when
+ *                p == 1, send-buffer index when p > 1),
+ *   tw_exp[i]  = e such that the output is multiplied by exp(-2 pi i e / n)
+ *                (-1 when the pass applies no twiddle).
+ * Arrays hold n/p entries each (caller-owned host memory).  *F_out receives F.
+ * Returns MOA_OK or an error code (same validation as moa_fft_plan_ex).
+ */
+int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opts, int pass,
+                          int64_t *in_idx, int64_t *out_idx, int64_t *tw_exp, int64_t *F_out);
+
 /* Thread-local description of the last error ("" if none). */
 const char *moa_fft_last_error(void);
 

@@ -17,7 +17,7 @@ import os
 
 from . import build as _build
 
-__all__ = ["Plan", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize",
+__all__ = ["Plan", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "lib_path", "load"]
 
 MODE_LIFTED, MODE_LITERAL, MODE_EMULATED = 0, 1, 2
@@ -47,7 +47,7 @@ class _Info(ctypes.Structure):
 EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host",
            "moa_fft_destroy", "moa_fft_set_stream", "moa_fft_plan_info", "moa_fft_last_error",
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
-           "moa_fft_version"]
+           "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass"]
 
 _lib = None
 
@@ -57,11 +57,11 @@ def lib_path() -> str:
 
 
 def load(build_if_needed: bool = True):
-    """Load libmoa_fft.so (building it with nvcc first if it is missing or stale)."""
+    """Load libmoa_fft.so (building it with nvcc first only if it is missing)."""
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_needed and _build.needs_build():
+    if build_if_needed and not os.path.exists(_build.LIB):
         _build.build()
     if not os.path.exists(_build.LIB):
         raise ImportError(f"{_build.LIB} is missing; run paper_0811_2535_b200/build.py (no CPU fallback)")
@@ -82,6 +82,10 @@ def load(build_if_needed: bool = True):
     lib.moa_dist_init.argtypes = [ci, ci, vp]
     lib.moa_gen_uniform.argtypes = [ctypes.c_uint64, i64, i64, i64, vp, vp]
     lib.moa_fft_version.restype = ctypes.c_char_p
+    lib.moa_fft_set_profiling.argtypes = [vp, ci]
+    lib.moa_fft_get_profile.argtypes = [vp, vp, ci]
+    lib.moa_fft_describe_pass.argtypes = [i64, ci, ci, ctypes.POINTER(_Options), ci, vp, vp, vp,
+                                          ctypes.POINTER(i64)]
     _lib = lib
     return lib
 
@@ -206,6 +210,27 @@ def gen_uniform(seed: int, count: int, out, first: int = 0, stride: int = 1, str
     if rc:
         _err(rc)
     return out
+
+
+def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
+    """Host-only index maps of one lifted pass (moa_fft_describe_pass; no GPU needed).
+
+    Returns (F, in_idx, out_idx, tw_exp) as numpy int64 arrays of n/p entries."""
+    import numpy as np
+    lib = load()
+    opt = _Options()
+    if lift:
+        opt.nlift = len(lift)
+        for i, f in enumerate(lift):
+            opt.lift[i] = int(f)
+    m = n // p
+    a, b, c = (np.empty(m, dtype=np.int64) for _ in range(3))
+    F = ctypes.c_int64(0)
+    rc = lib.moa_fft_describe_pass(int(n), int(p), int(rank), ctypes.byref(opt), int(pass_index),
+                                   a.ctypes.data, b.ctypes.data, c.ctypes.data, ctypes.byref(F))
+    if rc:
+        _err(rc)
+    return int(F.value), a, b, c
 
 
 def dist_init(group=None):

@@ -14,15 +14,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libmoa_fft.so")
+BUILD = os.path.join(HERE, "_build" + os.environ.get("MOA_BUILD_TAG", ""))
+LIB = os.environ.get("MOA_FFT_LIB") or os.path.join(HERE, "libmoa_fft.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+FLAGS = [*os.environ.get("MOA_NVCC_EXTRA", "").split(),
+         "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"]
 
-SOURCES = ["kernels.cu", "plan.cu", "dist.cu"]
+SOURCES = ["kernels.cu", "plan.cu", "dist.cu", "fused.cu"]
 INST_LOGF = list(range(1, 14))
 
 

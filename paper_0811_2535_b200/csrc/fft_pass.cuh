@@ -162,9 +162,58 @@ struct PassShape {
     static constexpr int MINB = (T * F <= 2048) ? 4 : ((T * F <= 4096) ? 2 : 1);
 };
 
+// Where one tile reads and writes (a persistent kernel retargets these per tile).
+//   ld: 0 = ld.global.nc, 1 = ld.global.cg (written earlier in the same launch),
+//       2 = ld.global.nc with an L2 evict_first policy (streamed once)
+//   st: 0 = st.global, 1 = st.global.cs (streaming), 2 = L2 evict_last policy
+struct TileIO {
+    const double2 *src;
+    double2 *dst;
+    int64_t in_shift, out_shift;
+    int ld, st;
+};
+
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_hint(const double2 *p, unsigned long long pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_hint(double2 *p, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ double2 ld_io(const TileIO &io, const double2 *p, unsigned long long pol) {
+#ifdef MOA_NO_HINTS
+    return io.ld == 1 ? __ldcg(p) : __ldg(p);
+#endif
+    if (io.ld == 1) return __ldcg(p);
+    if (io.ld == 2) return ld_hint(p, pol);
+    return __ldg(p);
+}
+__device__ __forceinline__ void st_io(const TileIO &io, double2 *p, double2 v, unsigned long long pol) {
+#ifdef MOA_NO_HINTS
+    *p = v;
+    return;
+#endif
+    if (io.st == 1) __stcs(p, v);
+    else if (io.st == 2) st_hint(p, v, pol);
+    else *p = v;
+}
+
 // One Stockham stage: Ns = product of the radices already applied.
 template <int F, int T, int NS, bool FIRST>
-__device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, int64_t in_base,
+__device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
+                                          int64_t in_base,
                                           int64_t k_base, uint64_t al_base, uint64_t be_base) {
     using SH = PassShape<F, T>;
     constexpr int R = SH::R;
@@ -176,6 +225,9 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     constexpr bool LAST = (NS * RS == F);
     const int tid = threadIdx.x;
 
+    unsigned long long pol = 0;
+    if (FIRST && io.ld == 2) pol = policy_evict_first();
+    if (LAST && io.st == 2) pol = policy_evict_last();
     int tt[M], jj[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -198,7 +250,8 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
             int f = jj[i] + r * NB;
             double2 val;
             if (FIRST) {
-                val = __ldg(d.src + in_base + (int64_t)tt[i] * d.in_t + (int64_t)f * d.in_f);
+                const double2 *p = io.src + (in_base - io.in_shift + (int64_t)tt[i] * d.in_t + (int64_t)f * d.in_f);
+                val = ld_io(io, p, pol);
                 if (d.conj_in) val.y = -val.y;
             } else {
                 val = sm[smem_idx<F, T>(tt[i], f)];
@@ -247,28 +300,27 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
                                ? (K & ((1ll << d.pack_lp) - 1)) * d.pack_chunk + (K >> d.pack_lp)
                                : K;
                 } else {
-                    addr = in_base + (int64_t)t * d.in_t + k * d.in_f;
+                    addr = in_base - io.out_shift + (int64_t)t * d.in_t + k * d.in_f;
                 }
-                d.dst[addr] = val;
+                st_io(io, io.dst + addr, val, pol);
             }
         }
     }
 }
 
 template <int F, int T, int NS>
-__device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, int64_t in_base,
-                                           int64_t k_base, uint64_t al_base, uint64_t be_base) {
+__device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
+                                           int64_t in_base, int64_t k_base, uint64_t al_base,
+                                           uint64_t be_base) {
     constexpr int REM = F / NS;
     constexpr int RS = REM >= 16 ? 16 : REM;
-    fft_stage<F, T, NS, NS == 1>(x, sm, d, in_base, k_base, al_base, be_base);
-    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS>(x, sm, d, in_base, k_base, al_base, be_base);
+    fft_stage<F, T, NS, NS == 1>(x, sm, d, io, in_base, k_base, al_base, be_base);
+    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS>(x, sm, d, io, in_base, k_base, al_base, be_base);
 }
 
+// one tile of T transforms; tile id -> (u, v, w) as documented in PassDesc
 template <int F, int T>
-__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
-    fft_pass_kernel(const PassDesc d) {
-    extern __shared__ double2 sm[];
-    int64_t b = blockIdx.x;
+__device__ __forceinline__ void tile_fft(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b) {
     const int64_t u = b % d.U;
     b /= d.U;
     const int64_t v = b % d.V;
@@ -278,7 +330,15 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     const uint64_t al_base = (uint64_t)d.a_c + (uint64_t)u * d.a_u + (uint64_t)v * d.a_v + (uint64_t)w * d.a_w;
     const uint64_t be_base = (uint64_t)d.b_c + (uint64_t)u * d.b_u + (uint64_t)v * d.b_v + (uint64_t)w * d.b_w;
     double2 x[PassShape<F, T>::R];
-    fft_stages<F, T, 1>(x, sm, d, in_base, k_base, al_base, be_base);
+    fft_stages<F, T, 1>(x, sm, d, io, in_base, k_base, al_base, be_base);
+}
+
+template <int F, int T>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_kernel(const PassDesc d) {
+    extern __shared__ double2 sm[];
+    TileIO io{d.src, d.dst, d.in_shift, d.out_shift, d.ld_hint, d.st_hint};
+    tile_fft<F, T>(sm, d, io, blockIdx.x);
 }
 
 template <int F, int T>

@@ -42,6 +42,30 @@ struct PassDesc {
     int in_tfast, out_tfast;// lane->(t, j) order of the global-facing stages
     int pack_lp;            // >= 0: send layout addr = (K & (P-1)) * pack_chunk + (K >> pack_lp)
     int64_t pack_chunk;
+    int64_t in_shift;       // subtracted from every input address (src is a window of the view)
+    int64_t out_shift;      // subtracted from every in-place output address (dst is a window)
+    int ld_hint, st_hint;   // TileIO ld/st cache modes for the global-facing stages
+};
+
+// L2-fused last two passes (persistent kernel): the middle pass of a 3-level
+// lifting writes row groups into an L2-resident scratch ring that the last
+// pass consumes, so HBM sees the traffic of two passes instead of three.
+struct FusedDesc {
+    PassDesc p2, p3;             // the middle and the last pass (src/dst windows set per group)
+    const int *items;            // schedule: item -> (kind << 30) | (group << 16) | tile
+    int64_t total_items;
+    unsigned long long *claim;   // work counter
+    unsigned long long *done2;   // per group: finished middle-pass tiles
+    unsigned long long *done3;   // per group: finished last-pass tiles
+    unsigned long long epoch;    // execute index (counters are monotone across executes)
+    int tiles2, tiles3;          // tiles per group of each kind
+    int groups, slots;
+    int64_t rows_per_group_elems;  // elements of one group in the scratch ring
+    double2 *scratch;            // slots * rows_per_group_elems
+    int64_t f2f3;                // elements per row (F2 * F3)
+    int p2_ld, scratch_st, p3_st, discard;  // cache hints (TileIO modes) and L2 discard of consumed scratch
+    const double2 *work;         // middle-pass input (whole view)
+    double2 *out;                // last-pass output
 };
 
 // host-side launchers (kernels.cu / fft_inst.cu)
@@ -50,6 +74,9 @@ size_t pass_smem_bytes(int logF, int T);
 int pass_threads(int logF, int T);
 cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaStream_t s);
 cudaError_t prepare_pass_kernels();    // raise the dynamic smem limits once
+int fused_supported(int logF2, int T2, int logF3, int T3);
+cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, int grid, cudaStream_t s);
+int fused_grid(int logF2, int T2, int logF3, int T3);
 
 cudaError_t launch_bitrev(const double2 *in, double2 *out, int t, int conj_in, cudaStream_t s);
 cudaError_t launch_radix2_stage(const double2 *in, double2 *out, int t, int q,

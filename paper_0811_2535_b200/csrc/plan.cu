@@ -106,6 +106,14 @@ struct moa_fft_plan_s {
     std::vector<PassPlan> passes;   // p == 1: all passes; p > 1: phase 1 for rank `rank`
     std::vector<std::vector<PassPlan>> rank_passes;  // emulated: phase 1 per virtual rank
     int64_t workspace_bytes = 0;
+    // L2-fused last two passes (fused.cu)
+    bool fused = false;
+    FusedDesc fd;
+    int fgrid = 0;
+    int *items = nullptr;
+    unsigned long long *counters = nullptr;
+    double2 *scratch = nullptr;
+    unsigned long long epoch = 0;
     // per-kernel event profiling (moa_fft_set_profiling)
     bool profiling = false;
     struct Slot {
@@ -143,6 +151,13 @@ static int default_lifting(int tl, int64_t *lift) {
         lift[0] = (int64_t)1 << tl;
         return 1;
     }
+    if (tl >= 20 && tl <= 16 + FMAX_LOG && env_int("MOA_FFT_FUSE", 1)) {
+        // <2^(tl-16), 256, 256>: the last two passes run L2-fused (fused.cu)
+        lift[0] = (int64_t)1 << (tl - 16);
+        lift[1] = 256;
+        lift[2] = 256;
+        return 3;
+    }
     if (tl <= 2 * (FMAX_LOG - 1) + 2) {   // two levels up to 2^26
         int a = tl / 2;
         lift[0] = (int64_t)1 << a;
@@ -165,7 +180,9 @@ static int default_lifting(int tl, int64_t *lift) {
 }
 
 static int choose_T(int logF, int64_t avail) {
-    int tf_max = env_int("MOA_FFT_TF", TF_MAX);
+    // tile size cap: long transforms take T*F = 8192 (one 128 KiB tile per SM);
+    // short ones 4096 (2-3 tiles per SM overlap memory and FP64 work)
+    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : 4096);
     if (tf_max > TF_MAX) tf_max = TF_MAX;
     int T = 1;
     while (T < 64 && ((int64_t)(2 * T) << logF) <= tf_max && 2 * T <= avail) T *= 2;
@@ -196,6 +213,8 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
         D.tw_lo = pl->tw_lo;
         D.tw_f = pl->tw_f;
         D.pack_lp = -1;
+        D.ld_hint = env_int("MOA_FFT_LDHINT", 0);
+        D.st_hint = env_int("MOA_FFT_STHINT", 0);
         D.conj_in = (i == 0 && pl->sign > 0);
         D.conj_out = 0;
         if (i < d - 1) {
@@ -315,6 +334,9 @@ static void free_plan(moa_fft_plan_s *pl) {
     cudaFree(pl->recv);
     cudaFree(pl->stage_in);
     cudaFree(pl->stage_out);
+    cudaFree(pl->items);
+    cudaFree(pl->counters);
+    cudaFree(pl->scratch);
     for (auto &r : pl->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -322,6 +344,94 @@ static void free_plan(moa_fft_plan_s *pl) {
     for (auto e : pl->pool) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete pl;
+}
+
+// Fuse the last two passes of a 3-level lifting through an L2-resident ring
+// (fused.cu) when a kernel for their (F, T) pair exists; otherwise keep them separate.
+static int setup_fused(moa_fft_plan_s *pl) {
+    PassPlan &p2 = pl->passes[1], &p3 = pl->passes[2];
+    if (!fused_supported(p2.logF, p2.T, p3.logF, p3.T)) return MOA_OK;
+    const int64_t F1 = pl->lift[0], F2 = pl->lift[1], F3 = pl->lift[2];
+    const int T3 = p3.T;
+    const int groups = (int)(F1 / T3);
+    const int tiles2 = (int)(F3 / p2.T) * T3;
+    const int tiles3 = (int)F2;
+    if (groups >= (1 << 14) || tiles2 >= (1 << 16) || tiles3 >= (1 << 16)) return MOA_OK;
+    int slots = env_int("MOA_FFT_SLOTS", 3), lag = env_int("MOA_FFT_LAG", 1);
+    if (lag < 0) lag = 0;
+    if (slots < lag + 1) slots = lag + 1;
+    if (slots > groups) slots = groups;
+    if (lag > slots - 1) lag = slots - 1;
+    std::vector<int> items;
+    for (int i = 0; i < groups + lag; ++i) {
+        if (i < groups)
+            for (int l = 0; l < tiles2; ++l) items.push_back((0 << 30) | (i << 16) | l);
+        if (i - lag >= 0)
+            for (int l = 0; l < tiles3; ++l) items.push_back((1 << 30) | ((i - lag) << 16) | l);
+    }
+    const int64_t group_elems = (int64_t)T3 * F2 * F3;
+    if (cudaMalloc((void **)&pl->items, items.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void **)&pl->counters, (1 + 2 * (size_t)groups) * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void **)&pl->scratch, (size_t)slots * group_elems * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOA_ERR_OOM, "fused-pass buffers allocation failed");
+    }
+    pl->workspace_bytes += items.size() * sizeof(int) + (1 + 2 * groups) * 8 + slots * group_elems * 16;
+    CUDA_TRY(cudaMemcpy(pl->items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(pl->counters, 0, (1 + 2 * (size_t)groups) * sizeof(unsigned long long)));
+    FusedDesc &fd = pl->fd;
+    memset(&fd, 0, sizeof fd);
+    fd.p2 = p2.d;
+    fd.p3 = p3.d;
+    fd.items = pl->items;
+    fd.total_items = (int64_t)items.size();
+    fd.claim = pl->counters;
+    fd.done2 = pl->counters + 1;
+    fd.done3 = pl->counters + 1 + groups;
+    fd.tiles2 = tiles2;
+    fd.tiles3 = tiles3;
+    fd.groups = groups;
+    fd.slots = slots;
+    fd.rows_per_group_elems = group_elems;
+    fd.scratch = pl->scratch;
+    fd.f2f3 = F2 * F3;
+    fd.p2_ld = env_int("MOA_FFT_P2LD", 0);
+    fd.scratch_st = env_int("MOA_FFT_SCRST", 2);
+    fd.p3_st = env_int("MOA_FFT_P3ST", 1);
+    fd.discard = env_int("MOA_FFT_DISCARD", 1);
+    pl->fgrid = fused_grid(p2.logF, p2.T, p3.logF, p3.T);
+    int gmax = env_int("MOA_FFT_FGRID", 0);
+    if (gmax > 0 && gmax < pl->fgrid) pl->fgrid = gmax;
+    if (pl->fgrid <= 0) return fail(MOA_ERR_CUDA, "fused kernel occupancy query failed");
+    pl->fused = true;
+    return MOA_OK;
+}
+
+// lifting <F1..Fd> from the options or the default table; sets pl->lift, pl->d
+static int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt) {
+    int tl = ilog2(pl->M);
+    const int p = pl->p;
+    if (opt && opt->nlift > 0) {
+        if (opt->nlift > 4) return fail(MOA_ERR_INVALID_ARG, "lifting depth %d > 4", opt->nlift);
+        int64_t prod = 1;
+        for (int i = 0; i < opt->nlift; ++i) {
+            int64_t F = opt->lift[i];
+            if (!pow2(F) || F < 2 || F > FMAX)
+                return fail(MOA_ERR_INVALID_ARG, "lifting factor %lld outside powers of two in [2, %d]",
+                            (long long)F, FMAX);
+            pl->lift[i] = F;
+            prod *= F;
+        }
+        if (prod != pl->M)
+            return fail(MOA_ERR_INVALID_ARG, "lifting product %lld != local length %lld", (long long)prod,
+                        (long long)pl->M);
+        pl->d = opt->nlift;
+    } else {
+        pl->d = default_lifting(tl, pl->lift);
+    }
+    if (p > 1 && pl->lift[0] < p && pl->d > 1)
+        return fail(MOA_ERR_INVALID_ARG, "first lifting factor %lld < p=%d", (long long)pl->lift[0], p);
+    return MOA_OK;
 }
 
 static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_plan_s **res) {
@@ -348,6 +458,7 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
         if (ws != p) return fail(MOA_ERR_INVALID_P, "p=%d differs from the world size %d", p, ws);
         rank = wr;
     }
+    int rc0 = MOA_OK;
     moa_fft_plan_s *pl = new moa_fft_plan_s();
     pl->n = n;
     pl->t = ilog2(n);
@@ -357,35 +468,9 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     pl->mode = mode;
     pl->M = n / p;
     CUDA_TRY(cudaGetDevice(&pl->device));
-    int tl = ilog2(pl->M);
-    if (opt && opt->nlift > 0) {
-        if (opt->nlift > 4) {
-            delete pl;
-            return fail(MOA_ERR_INVALID_ARG, "lifting depth %d > 4", opt->nlift);
-        }
-        int64_t prod = 1;
-        for (int i = 0; i < opt->nlift; ++i) {
-            int64_t F = opt->lift[i];
-            if (!pow2(F) || F < 2 || F > FMAX) {
-                delete pl;
-                return fail(MOA_ERR_INVALID_ARG, "lifting factor %lld outside powers of two in [2, %d]",
-                            (long long)F, FMAX);
-            }
-            pl->lift[i] = F;
-            prod *= F;
-        }
-        if (prod != pl->M) {
-            delete pl;
-            return fail(MOA_ERR_INVALID_ARG, "lifting product %lld != local length %lld", (long long)prod,
-                        (long long)pl->M);
-        }
-        pl->d = opt->nlift;
-    } else {
-        pl->d = default_lifting(tl, pl->lift);
-    }
-    if (p > 1 && pl->lift[0] < p && pl->d > 1) {
+    if ((rc0 = resolve_lifting(pl, opt)) != MOA_OK) {
         delete pl;
-        return fail(MOA_ERR_INVALID_ARG, "first lifting factor %lld < p=%d", (long long)pl->lift[0], p);
+        return rc0;
     }
     pl->chunks = 1;
 
@@ -449,6 +534,10 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
             }
     } else if (mode == MOA_MODE_LIFTED) {
         if ((rc = build_passes(pl, rank, p, pl->passes)) != MOA_OK) {
+            free_plan(pl);
+            return rc;
+        }
+        if (p == 1 && pl->d == 3 && env_int("MOA_FFT_FUSE", 1) && (rc = setup_fused(pl)) != MOA_OK) {
             free_plan(pl);
             return rc;
         }
@@ -527,6 +616,29 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
             CUDA_TRY(launch_radix2_stage(src, out, t, q, pl->tw_hi, pl->tw_lo, pl->hbits,
                                          (q == t) && pl->sign > 0, s));
         }
+        return MOA_OK;
+    }
+    if (pl->p == 1 && pl->fused) {
+        std::vector<PassPlan> first(pl->passes.begin(), pl->passes.begin() + 1);
+        PassDesc D = first[0].d;
+        D.src = in;
+        D.dst = pl->work;
+        {
+            char name[64];
+            snprintf(name, sizeof name, "pass0 fft_pass<F=%d,T=%d>", 1 << first[0].logF, first[0].T);
+            ProfScope sc(pl, name, 32 * pl->M);
+            CUDA_TRY(launch_pass(first[0].logF, first[0].T, D, first[0].tiles, s));
+        }
+        FusedDesc fd = pl->fd;
+        fd.work = pl->work;
+        fd.out = out;
+        fd.epoch = pl->epoch++;
+        char name[64];
+        snprintf(name, sizeof name, "pass1+2 fused<F=%d,T=%d|F=%d,T=%d>", 1 << pl->passes[1].logF,
+                 pl->passes[1].T, 1 << pl->passes[2].logF, pl->passes[2].T);
+        ProfScope sc(pl, name, 32 * pl->M);
+        CUDA_TRY(launch_fused(pl->passes[1].logF, pl->passes[1].T, pl->passes[2].logF, pl->passes[2].T, fd,
+                              pl->fgrid, s));
         return MOA_OK;
     }
     if (pl->p == 1) return run_passes(pl, pl->passes, in, out);
@@ -635,8 +747,8 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
         o->launches = pl->t + 1;
         o->hbm_bytes = 32 * pl->n * (pl->t + 1);
     } else if (pl->p == 1) {
-        o->launches = pl->d;
-        o->hbm_bytes = 32 * pl->n * pl->d;
+        o->launches = pl->fused ? pl->d - 1 : pl->d;
+        o->hbm_bytes = 32 * pl->n * (pl->fused ? pl->d - 1 : pl->d);
     } else {
         int per_rank = pl->d + 1;
         o->launches = pl->mode == MOA_MODE_EMULATED ? pl->p * per_rank : per_rank;
@@ -648,6 +760,61 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
 }
 
 const char *moa_fft_last_error(void) { return g_err.c_str(); }
+
+int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opts, int pass, int64_t *in_idx,
+                          int64_t *out_idx, int64_t *tw_exp, int64_t *F_out) {
+    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 34))
+        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 34", (long long)n);
+    if (!pow2(p) || p > 16 || n / p < p)
+        return fail(MOA_ERR_INVALID_P, "p=%d invalid for n=%lld (power of two, psize >= m, P:289)", p,
+                    (long long)n);
+    if (rank < 0 || rank >= p) return fail(MOA_ERR_INVALID_ARG, "rank %d outside [0, %d)", rank, p);
+    moa_fft_plan_s tmp;
+    tmp.n = n;
+    tmp.t = ilog2(n);
+    tmp.p = p;
+    tmp.M = n / p;
+    tmp.hbits = (tmp.t + 1) / 2;
+    int rc = resolve_lifting(&tmp, opts);
+    if (rc) return rc;
+    std::vector<PassPlan> ps;
+    if ((rc = build_passes(&tmp, rank, p, ps)) != MOA_OK) return rc;
+    if (pass < 0 || pass >= (int)ps.size())
+        return fail(MOA_ERR_INVALID_ARG, "pass %d outside [0, %d)", pass, (int)ps.size());
+    const PassPlan &pp = ps[pass];
+    const PassDesc &D = pp.d;
+    const int64_t F = (int64_t)1 << pp.logF;
+    if (F_out) *F_out = F;
+    int64_t i = 0;
+    for (int64_t b = 0; b < pp.tiles; ++b) {
+        int64_t bb = b;
+        const int64_t u = bb % D.U;
+        bb /= D.U;
+        const int64_t v = bb % D.V, w = bb / D.V;
+        const int64_t in_base = u * D.in_u + v * D.in_v + w * D.in_w;
+        const int64_t k_base = u * D.K_u + v * D.K_v + w * D.K_w;
+        const uint64_t al = (uint64_t)D.a_c + u * D.a_u + v * D.a_v + w * D.a_w;
+        const uint64_t be = (uint64_t)D.b_c + u * D.b_u + v * D.b_v + w * D.b_w;
+        for (int t = 0; t < pp.T; ++t)
+            for (int64_t f = 0; f < F; ++f, ++i) {
+                if (i >= tmp.M) return fail(MOA_ERR_INVALID_ARG, "internal: pass covers more than n/p");
+                in_idx[i] = in_base + t * D.in_t + f * D.in_f;
+                int64_t o;
+                if (D.last) {
+                    int64_t K = k_base + t * D.K_t + f * D.K_k;
+                    o = D.pack_lp >= 0 ? (K & (((int64_t)1 << D.pack_lp) - 1)) * D.pack_chunk + (K >> D.pack_lp) : K;
+                } else {
+                    o = in_base + t * D.in_t + f * D.in_f;
+                }
+                out_idx[i] = o;
+                tw_exp[i] = D.twiddle ? (int64_t)((al + t * (uint64_t)D.a_t + (be + t * (uint64_t)D.b_t) * (uint64_t)f) &
+                                                  D.nmask)
+                                      : -1;
+            }
+    }
+    if (i != tmp.M) return fail(MOA_ERR_INVALID_ARG, "internal: pass covers %lld of %lld", (long long)i, (long long)tmp.M);
+    return MOA_OK;
+}
 
 int moa_fft_set_profiling(moa_fft_plan_t pl, int enable) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");

@@ -139,8 +139,10 @@ def test_execute_host_end_to_end():
 
 def test_plan_info():
     info = moa.Plan(1 << 24).info()
-    assert info["passes"] == 2 and info["lift"] == [4096, 4096]
-    assert info["hbm_bytes"] == 32 * (1 << 24) * 2
+    assert info["passes"] == 3 and info["lift"] == [256, 256, 256]
+    assert info["hbm_bytes"] == 32 * (1 << 24) * 2   # last two passes L2-fused
+    info = moa.Plan(1 << 24, lift=[4096, 4096]).info()
+    assert info["passes"] == 2 and info["hbm_bytes"] == 32 * (1 << 24) * 2
     assert info["breakpoint"] == 25
     info = moa.Plan(1 << 30 if False else 1 << 27).info()
     assert info["passes"] == 3

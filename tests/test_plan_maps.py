@@ -1,0 +1,94 @@
+"""Host logic of the plan builder, checked on the CPU (no GPU needed).
+
+moa_fft_describe_pass exposes, for every lifted pass, the exact index maps and
+twiddle exponents the CUDA pass kernel uses (same PassDesc, same address
+arithmetic).  Replaying those maps with numpy's FFT for the F-point inner
+transforms must reproduce the oracle: this pins the lifting (reshape), the
+transposed store (Fig A.1 transpose+ravel), the inter-pass twiddles
+and, for p > 1, the rank twiddle + pack of Fig 4.4/5.9 and the cyclic output
+layout X[r + p*i].  The arithmetic here is test-side numpy;
+what is under test is the product's host-side index logic.
+"""
+import numpy as np
+import pytest
+
+import moa_inputs
+import oracle
+import paper_0811_2535_b200 as moa
+
+
+def replay_local(x_local, n, p, rank, lift=None):
+    """Run the local passes of one rank from their maps (numpy arithmetic)."""
+    m = n // p
+    k = 0
+    cur = np.asarray(x_local, dtype=np.complex128)
+    while True:
+        try:
+            F, ii, oi, tw = moa.describe_pass(n, p, rank, k, lift)
+        except moa.MoaError as e:
+            if "outside" in str(e) and k > 0:
+                break
+            raise
+        assert np.array_equal(np.sort(ii), np.arange(m)), "input map is not a permutation"
+        assert np.array_equal(np.sort(oi), np.arange(m)), "output map is not a permutation"
+        y = np.fft.fft(cur[ii].reshape(-1, F), axis=1).reshape(-1)
+        sel = tw >= 0
+        y[sel] *= np.exp(-2j * np.pi * (tw[sel].astype(np.float64) / n))
+        nxt = np.empty(m, dtype=np.complex128)
+        nxt[oi] = y
+        cur = nxt
+        k += 1
+    return cur
+
+
+def pcombine(recv, p):
+    """out[c + chunk*k2] = sum_s omega_p^(s*k2) recv[s*chunk + c] (Fig 5.7 cyclic phase, lifted)."""
+    chunk = recv.size // p
+    R = recv.reshape(p, chunk)
+    return np.fft.fft(R, axis=0).reshape(-1)
+
+
+@pytest.mark.parametrize("t,lift", [
+    (4, None), (10, None), (13, None), (14, None), (16, None), (20, None), (22, None),
+    (12, [64, 64]), (16, [16, 16, 256]), (18, [8, 32, 1024]), (20, [16, 16, 16, 256]),
+    (20, [1024, 1024]), (24, [256, 256, 256]), (24, [4096, 4096]),
+])
+def test_single_rank_maps_compose_to_fft(t, lift):
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    got = replay_local(x, n, 1, 0, lift)
+    assert oracle.rel_l2(got, oracle.fft(x, -1, threads=8)) <= 1e-13
+
+
+@pytest.mark.parametrize("t,p,lift", [(6, 2, None), (8, 8, None), (10, 4, None), (14, 2, None),
+                                      (16, 8, None), (20, 4, None), (21, 4, [32, 128, 128]),
+                                      (18, 8, [8, 32, 128])])
+def test_partitioned_maps_with_exchange(t, p, lift):
+    """Every rank's phase 1 from its maps, the Fig 5.9 exchange, then the P-point combine."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    ref = oracle.fft(x, -1, threads=8)
+    m = n // p
+    chunk = m // p
+    send = [replay_local(x[r::p], n, p, r, lift) for r in range(p)]
+    for d in range(p):
+        recv = np.concatenate([send[s][d * chunk:(d + 1) * chunk] for s in range(p)])
+        out = pcombine(recv, p)
+        assert oracle.rel_l2(out, ref[d::p]) <= 1e-13, (d, p)
+
+
+def test_column_pass_reads_contiguous_runs():
+    # middle/first passes read T adjacent columns: runs of T contiguous elements
+    F, ii, _, _ = moa.describe_pass(1 << 24, 1, 0, 0)
+    rows = ii.reshape(-1, F)            # one row per transform
+    T = 16
+    assert np.all(np.diff(rows[:T, 0]) == 1)   # T transforms of a tile = T adjacent columns
+
+
+def test_describe_pass_validation():
+    with pytest.raises(moa.MoaError):
+        moa.describe_pass(100, 1, 0, 0)
+    with pytest.raises(moa.MoaError):
+        moa.describe_pass(1 << 10, 1, 0, 5)
+    with pytest.raises(moa.MoaError):
+        moa.describe_pass(1 << 10, 4, 4, 0)
