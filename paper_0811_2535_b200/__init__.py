@@ -233,12 +233,12 @@ def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
     return int(F.value), a, b, c
 
 
-def dist_init(group=None):
-    """Create the library's NCCL communicator over torch.distributed's world (rank 0's id broadcast)."""
+def bcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates an ncclUniqueId (moa_dist_unique_id); torch.distributed broadcasts it."""
     import torch
     import torch.distributed as dist
     lib = load()
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rank = dist.get_rank(group)
     buf = (ctypes.c_char * 128)()
     if rank == 0:
         rc = lib.moa_dist_unique_id(buf)
@@ -248,7 +248,15 @@ def dist_init(group=None):
         else torch.device("cpu")
     t = torch.frombuffer(bytearray(bytes(buf)), dtype=torch.uint8).to(dev)
     dist.broadcast(t, 0, group=group)
-    ident = bytes(t.cpu().numpy().tobytes())
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def dist_init(group=None):
+    """Create the library's NCCL communicator over torch.distributed's world."""
+    import torch.distributed as dist
+    lib = load()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ident = bcast_unique_id(group)
     rc = lib.moa_dist_init(rank, world, ctypes.c_char_p(ident))
     if rc:
         _err(rc)

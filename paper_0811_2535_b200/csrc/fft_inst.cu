@@ -38,6 +38,53 @@ cudaError_t MOA_CAT(launch_pass_f, MOA_INST_LOGF)(int T, const PassDesc &d, int6
     }
 }
 
+// TMA-staged persistent variants: F >= 32, T*F <= 4096 (staging + exchange buffers fit)
+template <int T, int SRC>
+static constexpr bool tma_ok() {
+    return kF >= 32 && T * kF <= 4096 && T * kF >= 256;
+}
+
+cudaError_t MOA_CAT(launch_pass_tma_f, MOA_INST_LOGF)(int T, int src, const PassDesc &d, const CUtensorMap &map,
+                                                     int64_t tiles, int grid, cudaStream_t s) {
+#define MOA_TMA_CASE(TT)                                                                   \
+    if (T == TT) {                                                                         \
+        if constexpr (tma_ok<TT, 1>()) {                                                   \
+            if (src == 1) return launch_one_tma<kF, TT, 1>(d, map, tiles, grid, s);        \
+            if (src == 2) return launch_one_tma<kF, TT, 2>(d, map, tiles, grid, s);        \
+        }                                                                                  \
+        return cudaErrorInvalidValue;                                                      \
+    }
+    MOA_TMA_CASE(1)
+    MOA_TMA_CASE(2)
+    MOA_TMA_CASE(4)
+    MOA_TMA_CASE(8)
+    MOA_TMA_CASE(16)
+    MOA_TMA_CASE(32)
+    MOA_TMA_CASE(64)
+#undef MOA_TMA_CASE
+    return cudaErrorInvalidValue;
+}
+
+int MOA_CAT(grid_pass_tma_f, MOA_INST_LOGF)(int T, int src) {
+#define MOA_TMA_GRID(TT)                                                \
+    if (T == TT) {                                                      \
+        if constexpr (tma_ok<TT, 1>()) {                                \
+            if (src == 1) return grid_one_tma<kF, TT, 1>();             \
+            if (src == 2) return grid_one_tma<kF, TT, 2>();             \
+        }                                                               \
+        return 0;                                                       \
+    }
+    MOA_TMA_GRID(1)
+    MOA_TMA_GRID(2)
+    MOA_TMA_GRID(4)
+    MOA_TMA_GRID(8)
+    MOA_TMA_GRID(16)
+    MOA_TMA_GRID(32)
+    MOA_TMA_GRID(64)
+#undef MOA_TMA_GRID
+    return 0;
+}
+
 cudaError_t MOA_CAT(prepare_pass_f, MOA_INST_LOGF)() {
     cudaError_t e;
     if ((e = prepare_t<1>()) != cudaSuccess) return e;

@@ -19,6 +19,7 @@
 // conj_out flags), so every table is the omega^-e table.
 #pragma once
 #include "moa_internal.h"
+#include "tma.cuh"
 
 namespace moa {
 
@@ -170,7 +171,6 @@ struct TileIO {
     const double2 *src;
     double2 *dst;
     int64_t in_shift, out_shift;
-    int ld, st;
 };
 
 __device__ __forceinline__ unsigned long long policy_evict_first() {
@@ -192,28 +192,42 @@ __device__ __forceinline__ void st_hint(double2 *p, double2 v, unsigned long lon
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
                  : "memory");
 }
-__device__ __forceinline__ double2 ld_io(const TileIO &io, const double2 *p, unsigned long long pol) {
-#ifdef MOA_NO_HINTS
-    return io.ld == 1 ? __ldcg(p) : __ldg(p);
-#endif
-    if (io.ld == 1) return __ldcg(p);
-    if (io.ld == 2) return ld_hint(p, pol);
-    return __ldg(p);
+template <int LD>
+__device__ __forceinline__ double2 ld_io(const double2 *p, unsigned long long pol) {
+    if constexpr (LD == 1) return __ldcg(p);
+    else if constexpr (LD == 2) return ld_hint(p, pol);
+    else return __ldg(p);
 }
-__device__ __forceinline__ void st_io(const TileIO &io, double2 *p, double2 v, unsigned long long pol) {
-#ifdef MOA_NO_HINTS
-    *p = v;
-    return;
-#endif
-    if (io.st == 1) __stcs(p, v);
-    else if (io.st == 2) st_hint(p, v, pol);
+template <int ST>
+__device__ __forceinline__ void st_io(double2 *p, double2 v, unsigned long long pol) {
+    if constexpr (ST == 1) __stcs(p, v);
+    else if constexpr (ST == 2) st_hint(p, v, pol);
     else *p = v;
 }
 
+// Input staging layouts of a TMA-loaded tile (SRC != 0):
+//   SRC 1 (column tile, box {2T doubles, <=256 points, 1}):   [F][T]
+//   SRC 2 (row tile, boxes {<=128 points, T rows} side by side): [F/FB][T][FB], FB = min(F, 128)
+template <int F, int T, int SRC>
+__device__ __forceinline__ int stage_idx(int t, int f) {
+    if constexpr (SRC == 1) {
+        return f * T + t;
+    } else {
+        constexpr int FB = F < 128 ? F : 128;
+        return (f / FB) * (T * FB) + t * FB + (f % FB);
+    }
+}
+
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
 // One Stockham stage: Ns = product of the radices already applied.
-template <int F, int T, int NS, bool FIRST>
+//   SRC 0: the first stage gathers from global memory; SRC 1/2: from the TMA
+//   staging buffer `inbuf`, after which hook() runs (barrier + next prefetch).
+template <int F, int T, int NS, bool FIRST, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
 __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
-                                          int64_t in_base,
+                                          const double2 *inbuf, const Hook &hook, int64_t in_base,
                                           int64_t k_base, uint64_t al_base, uint64_t be_base) {
     using SH = PassShape<F, T>;
     constexpr int R = SH::R;
@@ -226,13 +240,14 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     const int tid = threadIdx.x;
 
     unsigned long long pol = 0;
-    if (FIRST && io.ld == 2) pol = policy_evict_first();
-    if (LAST && io.st == 2) pol = policy_evict_last();
+    if constexpr (FIRST && LD == 2) pol = policy_evict_first();
+    if constexpr (LAST && ST == 2) pol = policy_evict_last();
     int tt[M], jj[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         int b = tid + NT * i;
-        bool tfast = FIRST ? d.in_tfast : (LAST ? d.out_tfast : false);
+        bool tfast = FIRST ? (SRC == 1 ? true : (SRC == 2 ? false : (bool)d.in_tfast))
+                           : (LAST ? d.out_tfast : false);
         if (FIRST && LAST) tfast = d.in_tfast;
         if (tfast) {
             tt[i] = b % T;
@@ -249,9 +264,12 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         for (int r = 0; r < RS; ++r) {
             int f = jj[i] + r * NB;
             double2 val;
-            if (FIRST) {
+            if (FIRST && SRC != 0) {
+                val = inbuf[stage_idx<F, T, SRC>(tt[i], f)];
+                if (d.conj_in) val.y = -val.y;
+            } else if (FIRST) {
                 const double2 *p = io.src + (in_base - io.in_shift + (int64_t)tt[i] * d.in_t + (int64_t)f * d.in_f);
-                val = ld_io(io, p, pol);
+                val = ld_io<LD>(p, pol);
                 if (d.conj_in) val.y = -val.y;
             } else {
                 val = sm[smem_idx<F, T>(tt[i], f)];
@@ -259,6 +277,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
             x[i * RS + r] = val;
         }
     }
+    if constexpr (FIRST && SRC != 0) hook();
     // ---- twiddle + radix-RS butterflies in registers
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -302,25 +321,28 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
                 } else {
                     addr = in_base - io.out_shift + (int64_t)t * d.in_t + k * d.in_f;
                 }
-                st_io(io, io.dst + addr, val, pol);
+                st_io<ST>(io.dst + addr, val, pol);
             }
         }
     }
 }
 
-template <int F, int T, int NS>
+template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
 __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
-                                           int64_t in_base, int64_t k_base, uint64_t al_base,
-                                           uint64_t be_base) {
+                                           const double2 *inbuf, const Hook &hook, int64_t in_base,
+                                           int64_t k_base, uint64_t al_base, uint64_t be_base) {
     constexpr int REM = F / NS;
     constexpr int RS = REM >= 16 ? 16 : REM;
-    fft_stage<F, T, NS, NS == 1>(x, sm, d, io, in_base, k_base, al_base, be_base);
-    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS>(x, sm, d, io, in_base, k_base, al_base, be_base);
+    fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base, be_base);
+    if constexpr (NS * RS < F)
+        fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base,
+                                                    be_base);
 }
 
 // one tile of T transforms; tile id -> (u, v, w) as documented in PassDesc
-template <int F, int T>
-__device__ __forceinline__ void tile_fft(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b) {
+template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
+__device__ __forceinline__ void tile_fft(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b,
+                                         const double2 *inbuf = nullptr, const Hook &hook = Hook()) {
     const int64_t u = b % d.U;
     b /= d.U;
     const int64_t v = b % d.V;
@@ -330,14 +352,14 @@ __device__ __forceinline__ void tile_fft(double2 *sm, const PassDesc &d, const T
     const uint64_t al_base = (uint64_t)d.a_c + (uint64_t)u * d.a_u + (uint64_t)v * d.a_v + (uint64_t)w * d.a_w;
     const uint64_t be_base = (uint64_t)d.b_c + (uint64_t)u * d.b_u + (uint64_t)v * d.b_v + (uint64_t)w * d.b_w;
     double2 x[PassShape<F, T>::R];
-    fft_stages<F, T, 1>(x, sm, d, io, in_base, k_base, al_base, be_base);
+    fft_stages<F, T, 1, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base, be_base);
 }
 
 template <int F, int T>
 __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     fft_pass_kernel(const PassDesc d) {
     extern __shared__ double2 sm[];
-    TileIO io{d.src, d.dst, d.in_shift, d.out_shift, d.ld_hint, d.st_hint};
+    TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     tile_fft<F, T>(sm, d, io, blockIdx.x);
 }
 
@@ -355,6 +377,99 @@ cudaError_t prepare_one() {
         return cudaFuncSetAttribute(fft_pass_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SH::SMEM);
     return cudaSuccess;
+}
+
+}  // namespace moa
+
+namespace moa {
+
+// ---------------------------------------------------------------------------
+// Persistent TMA pass: one CTA per SM slot walks tiles blockIdx.x, +gridDim.x, ...
+// The tile is copied global -> shared by cp.async.bulk.tensor (one elected
+// thread, mbarrier completion); as soon as the first butterfly stage has read
+// it into registers the copy of the CTA's next tile is issued, so HBM reads
+// overlap the FP64 butterflies, the shared-memory exchanges and the stores.
+template <int F, int T, int SRC>
+struct TmaShape {
+    static constexpr int FB = SRC == 1 ? (F < 256 ? F : 256) : (F < 128 ? F : 128);   // points per box
+    static constexpr int NBOX = F / FB;
+    static constexpr unsigned BOX_BYTES = (unsigned)(FB * T * 16);
+    static constexpr size_t IN_BYTES = (size_t)T * F * 16;
+    static constexpr size_t SMEM = 128 + IN_BYTES + PassShape<F, T>::SMEM + 16;
+};
+
+template <int F, int T, int SRC>
+__device__ __forceinline__ void tma_issue_tile(const CUtensorMap *map, uint64_t *bar, double2 *inbuf,
+                                               const PassDesc &d, int64_t tile) {
+    using TS = TmaShape<F, T, SRC>;
+    int64_t b = tile;
+    const int u = (int)(b % d.U);
+    b /= d.U;
+    const int v = (int)(b % d.V);
+    const int w = (int)(b / d.V);
+    mbar_expect_tx(bar, TS::BOX_BYTES * TS::NBOX);
+#pragma unroll
+    for (int k = 0; k < TS::NBOX; ++k) {
+        if constexpr (SRC == 1)   // column tile: dims {2B doubles, F, A}
+            tma_load_3d(inbuf + k * TS::FB * T, map, bar, 2 * T * u, k * TS::FB, v);
+        else                      // row tile: dims {2F doubles, rows, V, W}
+            tma_load_4d(inbuf + k * TS::FB * T, map, bar, 2 * TS::FB * k, T * u, v, w);
+    }
+}
+
+template <int F, int T, int SRC>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, 1)
+    fft_pass_tma_kernel(const PassDesc d, const __grid_constant__ CUtensorMap tmap, int64_t tiles) {
+    extern __shared__ unsigned char smraw[];
+    double2 *inbuf = reinterpret_cast<double2 *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    double2 *work = inbuf + T * F;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(work + (PassShape<F, T>::SMEM / sizeof(double2)));
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    int64_t tile = blockIdx.x;
+    if (tid == 0 && tile < tiles) tma_issue_tile<F, T, SRC>(&tmap, bar, inbuf, d, tile);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    unsigned phase = 0;
+    for (; tile < tiles; tile += gridDim.x) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        const int64_t next = tile + gridDim.x;
+        auto hook = [&]() {
+            __syncthreads();   // every lane has its inputs in registers: the staging buffer is free
+            if (tid == 0 && next < tiles) {
+                fence_proxy_async();
+                tma_issue_tile<F, T, SRC>(&tmap, bar, inbuf, d, next);
+            }
+        };
+        tile_fft<F, T, SRC>(work, d, io, tile, inbuf, hook);
+    }
+}
+
+template <int F, int T, int SRC>
+cudaError_t launch_one_tma(const PassDesc &d, const CUtensorMap &map, int64_t tiles, int grid, cudaStream_t s) {
+    using TS = TmaShape<F, T, SRC>;
+    fft_pass_tma_kernel<F, T, SRC><<<grid, PassShape<F, T>::NT, TS::SMEM, s>>>(d, map, tiles);
+    return cudaGetLastError();
+}
+
+template <int F, int T, int SRC>
+int grid_one_tma() {
+    using TS = TmaShape<F, T, SRC>;
+    if (TS::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(fft_pass_tma_kernel<F, T, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TS::SMEM) != cudaSuccess)
+        return 0;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft_pass_tma_kernel<F, T, SRC>,
+                                                      PassShape<F, T>::NT, TS::SMEM) != cudaSuccess)
+        return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
 }
 
 }  // namespace moa

@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
                 if (threadIdx.x == 0) wait_geq(fd.done3 + (g - fd.slots), tgt3);
                 __syncthreads();
             }
-            TileIO io{fd.work, slot_ptr, 0, shift, fd.p2_ld, fd.scratch_st};
-            tile_fft<F2, T2>(sm, fd.p2, io, (int64_t)g * fd.tiles2 + tile);
+            TileIO io{fd.work, slot_ptr, 0, shift};
+            tile_fft<F2, T2, 0, NoHook, 0, 0>(sm, fd.p2, io, (int64_t)g * fd.tiles2 + tile);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
         } else {
             if (threadIdx.x == 0) wait_geq(fd.done2 + g, tgt2);
             __syncthreads();
-            TileIO io{slot_ptr, fd.out, shift, 0, 1, fd.p3_st};
-            tile_fft<F3, T3>(sm, fd.p3, io, (int64_t)g + (int64_t)(fd.groups) * tile);
+            TileIO io{slot_ptr, fd.out, shift, 0};
+            tile_fft<F3, T3, 0, NoHook, 1, 1>(sm, fd.p3, io, (int64_t)g + (int64_t)(fd.groups) * tile);
             __syncthreads();
             if (fd.discard) {
                 // the consumed scratch lines are dead: drop them from L2 without write-back.

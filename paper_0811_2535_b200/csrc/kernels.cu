@@ -48,6 +48,35 @@ cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaS
     }
 }
 
+int pass_tma_grid(int logF, int T, int src) {
+    switch (logF) {
+    case 5: return grid_pass_tma_f5(T, src);
+    case 6: return grid_pass_tma_f6(T, src);
+    case 7: return grid_pass_tma_f7(T, src);
+    case 8: return grid_pass_tma_f8(T, src);
+    case 9: return grid_pass_tma_f9(T, src);
+    case 10: return grid_pass_tma_f10(T, src);
+    case 11: return grid_pass_tma_f11(T, src);
+    case 12: return grid_pass_tma_f12(T, src);
+    default: return 0;
+    }
+}
+
+cudaError_t launch_pass_tma(int logF, int T, int src, const PassDesc &d, const CUtensorMap &map, int64_t tiles,
+                            int grid, cudaStream_t s) {
+    switch (logF) {
+    case 5: return launch_pass_tma_f5(T, src, d, map, tiles, grid, s);
+    case 6: return launch_pass_tma_f6(T, src, d, map, tiles, grid, s);
+    case 7: return launch_pass_tma_f7(T, src, d, map, tiles, grid, s);
+    case 8: return launch_pass_tma_f8(T, src, d, map, tiles, grid, s);
+    case 9: return launch_pass_tma_f9(T, src, d, map, tiles, grid, s);
+    case 10: return launch_pass_tma_f10(T, src, d, map, tiles, grid, s);
+    case 11: return launch_pass_tma_f11(T, src, d, map, tiles, grid, s);
+    case 12: return launch_pass_tma_f12(T, src, d, map, tiles, grid, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t prepare_pass_kernels() {
     cudaError_t (*fns[])() = {prepare_pass_f1, prepare_pass_f2, prepare_pass_f3, prepare_pass_f4,
                               prepare_pass_f5, prepare_pass_f6, prepare_pass_f7, prepare_pass_f8,

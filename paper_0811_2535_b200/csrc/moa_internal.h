@@ -1,6 +1,7 @@
 // moa_internal.h -- types shared by the host plan code and the CUDA kernels.
 // Not part of the public ABI (include/moa_fft.h is).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,7 +45,6 @@ struct PassDesc {
     int64_t pack_chunk;
     int64_t in_shift;       // subtracted from every input address (src is a window of the view)
     int64_t out_shift;      // subtracted from every in-place output address (dst is a window)
-    int ld_hint, st_hint;   // TileIO ld/st cache modes for the global-facing stages
 };
 
 // L2-fused last two passes (persistent kernel): the middle pass of a 3-level
@@ -63,7 +63,7 @@ struct FusedDesc {
     int64_t rows_per_group_elems;  // elements of one group in the scratch ring
     double2 *scratch;            // slots * rows_per_group_elems
     int64_t f2f3;                // elements per row (F2 * F3)
-    int p2_ld, scratch_st, p3_st, discard;  // cache hints (TileIO modes) and L2 discard of consumed scratch
+    int discard;                 // L2 discard of consumed scratch lines
     const double2 *work;         // middle-pass input (whole view)
     double2 *out;                // last-pass output
 };
@@ -74,6 +74,10 @@ size_t pass_smem_bytes(int logF, int T);
 int pass_threads(int logF, int T);
 cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaStream_t s);
 cudaError_t prepare_pass_kernels();    // raise the dynamic smem limits once
+// TMA-staged persistent pass (src 1: column tile, 2: row tile); grid 0 = unsupported
+int pass_tma_grid(int logF, int T, int src);
+cudaError_t launch_pass_tma(int logF, int T, int src, const PassDesc &d, const CUtensorMap &map, int64_t tiles,
+                            int grid, cudaStream_t s);
 int fused_supported(int logF2, int T2, int logF3, int T3);
 cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, int grid, cudaStream_t s);
 int fused_grid(int logF2, int T2, int logF3, int T3);
@@ -94,6 +98,9 @@ cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int
     namespace moa {                                                                         \
     cudaError_t launch_pass_f##f(int T, const PassDesc &d, int64_t tiles, cudaStream_t s);  \
     cudaError_t prepare_pass_f##f();                                                        \
+    cudaError_t launch_pass_tma_f##f(int T, int src, const PassDesc &d, const CUtensorMap &map, \
+                                     int64_t tiles, int grid, cudaStream_t s);              \
+    int grid_pass_tma_f##f(int T, int src);                                                 \
     }
 MOA_DECLARE_INST(1)
 MOA_DECLARE_INST(2)

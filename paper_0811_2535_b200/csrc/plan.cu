@@ -84,7 +84,88 @@ struct PassPlan {
     int logF, T;
     int64_t tiles;
     PassDesc d;  // src/dst patched at execute
+    // TMA-staged persistent variant (0 = plain kernel, 1 = column tile, 2 = row tile)
+    int tma = 0;
+    int tma_grid = 0;
+    CUtensorMap map;
+    const void *map_base = nullptr;
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// The box geometry must match TmaShape / tma_issue_tile in fft_pass.cuh.
+static int encode_pass_map(PassPlan &pp, const void *base) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const PassDesc &D = pp.d;
+    const uint64_t F = 1ull << pp.logF, T = pp.T;
+    cuuint64_t dims[4], strides[3];
+    cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+    cuuint32_t rank;
+    if (pp.tma == 1) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
+        const uint64_t B = (uint64_t)D.in_f, A = (uint64_t)D.V;
+        rank = 3;
+        dims[0] = 2 * B;
+        dims[1] = F;
+        dims[2] = A;
+        strides[0] = 16 * B;
+        strides[1] = 16 * F * B;
+        box[0] = (cuuint32_t)(2 * T);
+        box[1] = (cuuint32_t)(F < 256 ? F : 256);
+        box[2] = 1;
+    } else {             // row tile: dims {2F doubles, rows (u*T + t), V, W}
+        const uint64_t rows = (uint64_t)D.U * T, V = (uint64_t)D.V, W = (uint64_t)(pp.tiles / (D.U * D.V));
+        rank = 4;
+        dims[0] = 2 * F;
+        dims[1] = rows;
+        dims[2] = V;
+        dims[3] = W;
+        strides[0] = 16 * (uint64_t)D.in_t;
+        strides[1] = 16 * (uint64_t)(D.in_v ? D.in_v : D.in_t * rows);
+        strides[2] = 16 * (uint64_t)(D.in_w ? D.in_w : D.in_t * rows * V);
+        box[0] = (cuuint32_t)(F < 128 ? 2 * F : 256);
+        box[1] = (cuuint32_t)T;
+        box[2] = 1;
+        box[3] = 1;
+    }
+    CUresult r = enc(&pp.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void *>(base), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for pass F=%llu T=%llu", (int)r,
+                                       (unsigned long long)F, (unsigned long long)T);
+    pp.map_base = base;
+    return MOA_OK;
+}
+
+// choose the TMA-staged variant when it exists for this (F, T, layout)
+static void choose_tma(PassPlan &pp) {
+    pp.tma = 0;
+    if (!getenv("MOA_FFT_TMA") ? false : atoi(getenv("MOA_FFT_TMA")) == 0) return;
+    const PassDesc &D = pp.d;
+    int src = 0;
+    if (!D.last && D.in_t == 1 && pp.T >= 2) src = 1;
+    else if (D.last && D.in_f == 1) src = 2;
+    if (!src) return;
+    int g = pass_tma_grid(pp.logF, pp.T, src);
+    if (g <= 0) return;
+    pp.tma = src;
+    pp.tma_grid = g;
+}
 
 }  // namespace moa
 
@@ -213,8 +294,6 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
         D.tw_lo = pl->tw_lo;
         D.tw_f = pl->tw_f;
         D.pack_lp = -1;
-        D.ld_hint = env_int("MOA_FFT_LDHINT", 0);
-        D.st_hint = env_int("MOA_FFT_STHINT", 0);
         D.conj_in = (i == 0 && pl->sign > 0);
         D.conj_out = 0;
         if (i < d - 1) {
@@ -395,9 +474,6 @@ static int setup_fused(moa_fft_plan_s *pl) {
     fd.rows_per_group_elems = group_elems;
     fd.scratch = pl->scratch;
     fd.f2f3 = F2 * F3;
-    fd.p2_ld = env_int("MOA_FFT_P2LD", 0);
-    fd.scratch_st = env_int("MOA_FFT_SCRST", 2);
-    fd.p3_st = env_int("MOA_FFT_P3ST", 1);
     fd.discard = env_int("MOA_FFT_DISCARD", 1);
     pl->fgrid = fused_grid(p2.logF, p2.T, p3.logF, p3.T);
     int gmax = env_int("MOA_FFT_FGRID", 0);
@@ -532,11 +608,14 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
                 free_plan(pl);
                 return rc;
             }
+        for (auto &rp : pl->rank_passes)
+            for (auto &pp : rp) choose_tma(pp);
     } else if (mode == MOA_MODE_LIFTED) {
         if ((rc = build_passes(pl, rank, p, pl->passes)) != MOA_OK) {
             free_plan(pl);
             return rc;
         }
+        for (auto &pp : pl->passes) choose_tma(pp);
         if (p == 1 && pl->d == 3 && env_int("MOA_FFT_FUSE", 1) && (rc = setup_fused(pl)) != MOA_OK) {
             free_plan(pl);
             return rc;
@@ -583,20 +662,36 @@ struct ProfScope {
     }
 };
 
+// launch one pass (plain or TMA-staged) from src to dst
+static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, double2 *dst) {
+    PassDesc D = pp.d;
+    D.src = src;
+    D.dst = dst;
+    char name[64];
+    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>", idx, pp.tma ? "_tma" : "", 1 << pp.logF, pp.T);
+    ProfScope ps_(pl, name, 32 * pl->M);
+    cudaError_t e;
+    if (pp.tma) {
+        if (pp.map_base != (const void *)src) {
+            int rc = encode_pass_map(pp, src);
+            if (rc) return rc;
+        }
+        e = launch_pass_tma(pp.logF, pp.T, pp.tma, D, pp.map, pp.tiles, pp.tma_grid, pl->stream);
+    } else {
+        e = launch_pass(pp.logF, pp.T, D, pp.tiles, pl->stream);
+    }
+    if (e != cudaSuccess)
+        return fail(MOA_ERR_CUDA, "pass %d (F=2^%d, T=%d, tma=%d) launch failed: %s", idx, pp.logF, pp.T, pp.tma,
+                    cudaGetErrorString(e));
+    return MOA_OK;
+}
+
 // run the lifted passes of one (virtual) rank: in -> [work] -> out
 static int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in, double2 *out) {
     const int d = (int)ps.size();
     for (int i = 0; i < d; ++i) {
-        PassDesc D = ps[i].d;
-        D.src = (i == 0) ? in : pl->work;
-        D.dst = (i == d - 1) ? out : pl->work;
-        char name[64];
-        snprintf(name, sizeof name, "pass%d fft_pass<F=%d,T=%d>", i, 1 << ps[i].logF, ps[i].T);
-        ProfScope ps_(pl, name, 32 * pl->M);
-        cudaError_t e = launch_pass(ps[i].logF, ps[i].T, D, ps[i].tiles, pl->stream);
-        if (e != cudaSuccess)
-            return fail(MOA_ERR_CUDA, "pass %d (F=2^%d, T=%d) launch failed: %s", i, ps[i].logF, ps[i].T,
-                        cudaGetErrorString(e));
+        int rc = launch_pp(pl, ps[i], i, (i == 0) ? in : pl->work, (i == d - 1) ? out : pl->work);
+        if (rc) return rc;
     }
     return MOA_OK;
 }
@@ -619,16 +714,8 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
         return MOA_OK;
     }
     if (pl->p == 1 && pl->fused) {
-        std::vector<PassPlan> first(pl->passes.begin(), pl->passes.begin() + 1);
-        PassDesc D = first[0].d;
-        D.src = in;
-        D.dst = pl->work;
-        {
-            char name[64];
-            snprintf(name, sizeof name, "pass0 fft_pass<F=%d,T=%d>", 1 << first[0].logF, first[0].T);
-            ProfScope sc(pl, name, 32 * pl->M);
-            CUDA_TRY(launch_pass(first[0].logF, first[0].T, D, first[0].tiles, s));
-        }
+        int rc0 = launch_pp(pl, pl->passes[0], 0, in, pl->work);
+        if (rc0) return rc0;
         FusedDesc fd = pl->fd;
         fd.work = pl->work;
         fd.out = out;

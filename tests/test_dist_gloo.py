@@ -1,0 +1,98 @@
+"""World-size-2 gloo tests of the multi-process host path (CPU, no GPU).
+
+* the NCCL unique id made by the library on rank 0 reaches rank 1 intact through
+  torch.distributed (the rendezvous dist_init uses);
+* the partitioned plan's host maps (moa_fft_describe_pass: local lifted passes,
+  rank twiddle omega_n^(r*K), pack to [dst][K/p]) driven through a REAL two-process
+  exchange (gloo all_to_all_single, the S7 step) and the P-point combine give each
+  rank X[r + p*i] of the oracle;
+* bench.py --impl reference under torchrun: rank 0 prints the JSON line, rank 1 exits 0.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, t, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import moa_inputs
+        import oracle
+        import paper_0811_2535_b200 as moa
+        from test_plan_maps import pcombine, replay_local
+
+        ident = moa.bcast_unique_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, ident)
+        same_id = all(i == ids[0] for i in ids) and len(ident) == 128 and any(ident)
+
+        n = 1 << t
+        p = world
+        m = n // p
+        chunk = m // p
+        x_local = moa_inputs.rank_slice(t, rank, p)
+        send = replay_local(x_local, n, p, rank)                 # S5 + S6 from the product's maps
+        recv = torch.empty(2 * m, dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(send.view(np.float64).copy()),
+                               [2 * chunk] * p, [2 * chunk] * p)  # S7 over a real process boundary
+        out = pcombine(recv.numpy().view(np.complex128), p)        # S8
+        ref = oracle.fft(moa_inputs.signal_for(t), -1)[rank::p]
+        err = oracle.rel_l2(out, ref)
+        q.put((rank, same_id, err))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, False, repr(e)))
+
+
+@pytest.mark.parametrize("t", [10, 16])
+def test_two_rank_exchange_over_gloo(t):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, t, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, same_id, err in res:
+        assert not isinstance(err, str), err
+        assert same_id, "unique id differs across ranks"
+        assert err <= 1e-13, (rank, err)
+
+
+def test_bench_reference_arm_torchrun_two_ranks():
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "2", "--warmup", "3", "--t", "12"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
+    assert rec["cpu_baseline"]["kind"] == "oracle"
+    assert rec["e2e"]["h2d_bytes_per_step"] == 0

@@ -43,7 +43,35 @@ def time_plan(t, lift, reps=10, mode=moa.MODE_LIFTED, flush=True):
             "tf": os.environ.get("MOA_FFT_TF", "8192")}
 
 
+def calibrate():
+    """copy bandwidth (read+write bytes) of a 1 GiB tensor and the SM clock: box sanity check."""
+    a = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    for _ in range(3):
+        b.copy_(a)
+    ts = []
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    clk = None
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        clk = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:
+        pass
+    del a, b
+    return {"copy_GBps": round(2 * (1 << 30) / min(ts) / 1e9, 1), "sm_mhz": clk}
+
+
 if __name__ == "__main__":
+    print(json.dumps({"calibration": calibrate()}), flush=True)
     t = int(sys.argv[1])
     for spec in sys.argv[2:] or [""]:
         if spec == "literal":
