@@ -36,7 +36,7 @@ extern "C" {
 
 enum {
     MOA_OK = 0,
-    MOA_ERR_INVALID_N = -1,    /* n is not 2^t with 1 <= t <= 34                       */
+    MOA_ERR_INVALID_N = -1,    /* n is not 2^t with 1 <= t <= 32                       */
     MOA_ERR_INVALID_P = -2,    /* p not a power of two, p != world size, or n/p < p */
     MOA_ERR_INVALID_SIGN = -3, /* sign not -1 or +1                                    */
     MOA_ERR_ALIGN = -4,        /* a device pointer is NULL or not 16-byte aligned        */
@@ -86,7 +86,8 @@ typedef struct {
 
 /*
  * Create a plan for an n-point transform over p ranks.
- *   n    = 2^t, 1 <= t <= 34 (Fig 2.1 input "n = 2^t, t >= 1").
+ *   n    = 2^t, 1 <= t <= 32 (Fig 2.1 input "n = 2^t, t >= 1"; 2^32 complex128
+ *          = 64 GiB per buffer is beyond one 180 GB B200 once in/out/scratch are counted).
  *   p    = 1, or the world size given to moa_dist_init (a power of two, the paper's m)
  *          with n/p >= p (psize >= m).
  *   sign = -1 (forward, conventional) or +1 (the paper's literal EXP(+2*pi*i*row/L)).

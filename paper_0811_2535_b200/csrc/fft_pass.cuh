@@ -88,28 +88,29 @@ __device__ __forceinline__ void dft_reg(double2 *v) {
 
 // omega_n^e from the two-level table: hi[e >> h] * lo[e & (2^h - 1)]
 __device__ __forceinline__ double2 tw2(const double2 *__restrict__ hi, const double2 *__restrict__ lo,
-                                       uint64_t e, int h) {
-    return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((1ull << h) - 1))));
+                                       uint32_t e, int h) {
+    return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((1u << h) - 1))));
 }
 
 // q[r] = omega^(e0 + r*delta) for r < RS, from 1 + log2(RS) table lookups and
 // at most log2(RS) products per entry.
 template <int RS>
-__device__ __forceinline__ void twiddle_run(double2 *q, const PassDesc &d, uint64_t e0, uint64_t delta) {
-    q[0] = tw2(d.tw_hi, d.tw_lo, e0 & d.nmask, d.hbits);
+__device__ __forceinline__ void twiddle_run(double2 *q, const PassDesc &d, uint32_t e0, uint32_t delta) {
+    const uint32_t nm = (uint32_t)d.nmask;
+    q[0] = tw2(d.tw_hi, d.tw_lo, e0 & nm, d.hbits);
     if (RS == 1) return;
-    double2 p1 = tw2(d.tw_hi, d.tw_lo, delta & d.nmask, d.hbits);
+    double2 p1 = tw2(d.tw_hi, d.tw_lo, delta & nm, d.hbits);
     q[1] = cmul(q[0], p1);
     if (RS == 2) return;
-    double2 p2 = tw2(d.tw_hi, d.tw_lo, (2 * delta) & d.nmask, d.hbits);
+    double2 p2 = tw2(d.tw_hi, d.tw_lo, (2 * delta) & nm, d.hbits);
     q[2] = cmul(q[0], p2);
     q[3] = cmul(q[1], p2);
     if (RS == 4) return;
-    double2 p4 = tw2(d.tw_hi, d.tw_lo, (4 * delta) & d.nmask, d.hbits);
+    double2 p4 = tw2(d.tw_hi, d.tw_lo, (4 * delta) & nm, d.hbits);
 #pragma unroll
     for (int r = 4; r < 8 && r < RS; ++r) q[r] = cmul(q[r - 4], p4);
     if (RS == 8) return;
-    double2 p8 = tw2(d.tw_hi, d.tw_lo, (8 * delta) & d.nmask, d.hbits);
+    double2 p8 = tw2(d.tw_hi, d.tw_lo, (8 * delta) & nm, d.hbits);
 #pragma unroll
     for (int r = 8; r < RS; ++r) q[r] = cmul(q[r - 8], p8);
 }
@@ -150,8 +151,15 @@ __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restr
 template <int F, int T>
 __device__ __forceinline__ int smem_idx(int t, int f) {
     constexpr int PAD = T == 1 ? 0 : (T == 2 ? 4 : (T == 4 ? 2 : 1));
-    int s = ((f >> 3) ^ (f >> 6) ^ (f >> 9) ^ (f >> 12)) & 7;
+    int s = ((f >> 3) ^ (f >> 6) ^ (f >> 9) ^ (f >> 12)) & 7;   // == swz(f)
     return t * (F + PAD) + (f ^ s);
+}
+
+// radix of the last Stockham stage of an F-point transform (radix 16 first, remainder last)
+__host__ __device__ constexpr int lrs(int F) {
+    int ns = 1;
+    while (F / ns > 16) ns *= 16;
+    return F / ns;
 }
 
 template <int F, int T>
@@ -159,8 +167,17 @@ struct PassShape {
     static constexpr int R = F >= 16 ? 16 : F;   // points per thread
     static constexpr int NT = T * F / R;         // threads per CTA
     static constexpr int PAD = T == 1 ? 0 : (T == 2 ? 4 : (T == 4 ? 2 : 1));
-    static constexpr size_t SMEM = (F <= 16) ? 0 : (size_t)T * (F + PAD) * sizeof(double2);
-    static constexpr int MINB = (T * F <= 2048) ? 4 : ((T * F <= 4096) ? 2 : 1);
+    // last-stage geometry (for the per-tile twiddle tables)
+    static constexpr int LRS = lrs(F);
+    static constexpr int LNB = F / LRS;
+    static constexpr size_t XCH = (F <= 16) ? 0 : (size_t)T * (F + PAD) * sizeof(double2);   // exchange buffer
+    static constexpr size_t TWA = (size_t)T * (LNB + 1) * sizeof(double2);   // A[t][j] = w^(al_t + be_t j)
+    static constexpr size_t TWB = (size_t)T * (LRS + 1) * sizeof(double2);   // B[t][r] = w^(be_t NB r)
+    static constexpr size_t SMEM = XCH + TWA + TWB;
+#ifndef MOA_MINB_2048
+#define MOA_MINB_2048 4
+#endif
+    static constexpr int MINB = (T * F <= 2048) ? MOA_MINB_2048 : ((T * F <= 4096) ? 2 : 1);
 };
 
 // Where one tile reads and writes (a persistent kernel retargets these per tile).
@@ -222,13 +239,64 @@ struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
 
+// XOR-fold swizzle of a row-local point index (see smem_idx)
+__host__ __device__ constexpr int swz(int f) { return ((f >> 3) ^ (f >> 6) ^ (f >> 9) ^ (f >> 12)) & 7; }
+
+// flip the sign of the imaginary part when mask = 0x80000000 (conj without a select)
+__device__ __forceinline__ double2 conj_mask(double2 v, unsigned mask) {
+    v.y = __hiloint2double(__double2hiint(v.y) ^ (int)mask, __double2loint(v.y));
+    return v;
+}
+
+// Per-tile values shared by the stages of one tile.
+struct TileCtx {
+    const double2 *in;   // src + tile input base  (element (t, f) at in[t*in_t + f*in_f])
+    double2 *out;        // dst + tile output base (element (t, k) at out[t*out_t + k*out_k])
+    int64_t k_base;      // general pack path only
+    uint32_t al, be;     // twiddle exponent: omega_n^(al + a_t*t + (be + b_t*t)*k)
+    const double2 *twa;  // shared A[t][j], pitch LNB+1
+    const double2 *twb;  // shared B[t][r], pitch LRS+1
+};
+
+// omega_n^e = exp(-2 pi i e / n) evaluated directly: sincospi of the exact
+// rational -2e/n (no table, no memory latency; CUDA's sincospi is within 1 ulp)
+__device__ __forceinline__ double2 root_pi(uint32_t e, int t) {
+    double s, c;
+    sincospi(-ldexp((double)e, 1 - t), &s, &c);
+    return make_double2(c, s);
+}
+
+// Build the tile's twiddle tables: omega^(al_t + be_t*(j + r*NB)) = A[t][j] * B[t][r]
+// (computed at tile start; the stages' barriers publish them).
+template <int F, int T>
+__device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 *twa, double2 *twb, uint32_t al,
+                                                     uint32_t be) {
+    using SH = PassShape<F, T>;
+    constexpr int NB = SH::LNB, RS = SH::LRS;
+    const uint32_t nm = (uint32_t)d.nmask;
+    for (int i = threadIdx.x; i < T * (NB + RS); i += SH::NT) {
+        if (i < T * NB) {
+            const int t = i / NB, j = i % NB;
+            const uint32_t a = al + (uint32_t)t * (uint32_t)d.a_t, b = be + (uint32_t)t * (uint32_t)d.b_t;
+            twa[t * (NB + 1) + j] = root_pi((a + b * (uint32_t)j) & nm, d.tbits);
+        } else {
+            const int k = i - T * NB, t = k / RS, r = k % RS;
+            const uint32_t b = be + (uint32_t)t * (uint32_t)d.b_t;
+            twb[t * (RS + 1) + r] = root_pi((b * (uint32_t)(NB * r)) & nm, d.tbits);
+        }
+    }
+}
+
 // One Stockham stage: Ns = product of the radices already applied.
 //   SRC 0: the first stage gathers from global memory; SRC 1/2: from the TMA
 //   staging buffer `inbuf`, after which hook() runs (barrier + next prefetch).
+// Address arithmetic is split into a per-butterfly part and compile-time
+// per-point constants: global addresses are base + r*(NB*stride); shared
+// addresses use phys(j + r*NB) = (j ^ swz(j) ^ swz(r*NB)) + r*NB (the XOR fold is
+// linear over the disjoint bit fields of j and r*NB).
 template <int F, int T, int NS, bool FIRST, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
-__device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
-                                          const double2 *inbuf, const Hook &hook, int64_t in_base,
-                                          int64_t k_base, uint64_t al_base, uint64_t be_base) {
+__device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
+                                          const double2 *inbuf, const Hook &hook) {
     using SH = PassShape<F, T>;
     constexpr int R = SH::R;
     constexpr int NT = SH::NT;
@@ -237,6 +305,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     constexpr int NB = F / RS;                 // butterflies per transform
     constexpr int M = R / RS;                  // butterflies per thread
     constexpr bool LAST = (NS * RS == F);
+    constexpr int ROW = F + SH::PAD;           // shared row pitch
     const int tid = threadIdx.x;
 
     unsigned long long pol = 0;
@@ -247,8 +316,9 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     for (int i = 0; i < M; ++i) {
         int b = tid + NT * i;
         bool tfast = FIRST ? (SRC == 1 ? true : (SRC == 2 ? false : (bool)d.in_tfast))
-                           : (LAST ? d.out_tfast : false);
-        if (FIRST && LAST) tfast = d.in_tfast;
+                           : (LAST ? (bool)d.out_tfast : false);
+        if (FIRST && LAST) tfast = SRC == 1 ? true : (SRC == 2 ? false : (bool)d.in_tfast);
+        if (T == 1) tfast = false;
         if (tfast) {
             tt[i] = b % T;
             jj[i] = b / T;
@@ -257,102 +327,128 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
             jj[i] = b % NB;
         }
     }
-    // ---- gather inputs
+    // ---- gather inputs (the first stage then builds the tile's twiddle tables while
+    //      its loads are in flight)
+    if constexpr (FIRST && SRC == 0) {
+        const unsigned cm = d.conj_in ? 0x80000000u : 0u;
+        const int64_t sf = (int64_t)NB * d.in_f;
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
+        for (int i = 0; i < M; ++i) {
+            const double2 *p = c.in + (int64_t)tt[i] * d.in_t + (int64_t)jj[i] * d.in_f;
 #pragma unroll
-        for (int r = 0; r < RS; ++r) {
-            int f = jj[i] + r * NB;
-            double2 val;
-            if (FIRST && SRC != 0) {
-                val = inbuf[stage_idx<F, T, SRC>(tt[i], f)];
-                if (d.conj_in) val.y = -val.y;
-            } else if (FIRST) {
-                const double2 *p = io.src + (in_base - io.in_shift + (int64_t)tt[i] * d.in_t + (int64_t)f * d.in_f);
-                val = ld_io<LD>(p, pol);
-                if (d.conj_in) val.y = -val.y;
+            for (int r = 0; r < RS; ++r) x[i * RS + r] = conj_mask(ld_io<LD>(p + r * sf, pol), cm);
+        }
+        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
+    } else if constexpr (FIRST) {
+        const unsigned cm = d.conj_in ? 0x80000000u : 0u;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int r = 0; r < RS; ++r)
+                x[i * RS + r] = conj_mask(inbuf[stage_idx<F, T, SRC>(tt[i], jj[i] + r * NB)], cm);
+        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        hook();
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const int j = jj[i];
+            if constexpr (NB >= 8) {
+                const int rowoff = tt[i] * ROW, pj = j ^ swz(j);
+#pragma unroll
+                for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[rowoff + ((pj ^ swz(r * NB)) + r * NB)];
             } else {
-                val = sm[smem_idx<F, T>(tt[i], f)];
+#pragma unroll
+                for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[smem_idx<F, T>(tt[i], j + r * NB)];
             }
-            x[i * RS + r] = val;
         }
     }
-    if constexpr (FIRST && SRC != 0) hook();
     // ---- twiddle + radix-RS butterflies in registers
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         if (NS > 1) stage_twiddle<RS>(x + i * RS, d.tw_f, (jj[i] % NS) * (FMAX / (NS * RS)));
         dft_reg<RS>(x + i * RS);
     }
-    if (!LAST) {
+    if constexpr (!LAST) {
         if (!FIRST) __syncthreads();   // every lane has read before anyone overwrites
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            int j = jj[i];
-            int base = (j / NS) * NS * RS + (j % NS);
+            const int j = jj[i];
+            const int base = (j / NS) * NS * RS + (j % NS);
+            if constexpr (NS >= 8) {
+                const int rowoff = tt[i] * ROW, pb = base ^ swz(base);
 #pragma unroll
-            for (int r = 0; r < RS; ++r) sm[smem_idx<F, T>(tt[i], base + r * NS)] = x[i * RS + r];
+                for (int r = 0; r < RS; ++r) sm[rowoff + ((pb ^ swz(r * NS)) + r * NS)] = x[i * RS + r];
+            } else if constexpr (NS == 1 && RS >= 8) {
+                const int pb = tt[i] * ROW + base;
+                const int sb = swz(base);
+#pragma unroll
+                for (int r = 0; r < RS; ++r) sm[pb + (r ^ sb ^ swz(r))] = x[i * RS + r];
+            } else {
+#pragma unroll
+                for (int r = 0; r < RS; ++r) sm[smem_idx<F, T>(tt[i], base + r * NS)] = x[i * RS + r];
+            }
         }
         __syncthreads();
     } else {
+        const unsigned cm = d.conj_out ? 0x80000000u : 0u;
+        const int64_t so = (int64_t)NB * d.out_k;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const int t = tt[i], j = jj[i];
             double2 *v = x + i * RS;
             if (d.twiddle) {
-                uint64_t al = al_base + (uint64_t)t * (uint64_t)d.a_t;
-                uint64_t be = be_base + (uint64_t)t * (uint64_t)d.b_t;
-                double2 q[RS];
-                twiddle_run<RS>(q, d, al + be * (uint64_t)j, be * (uint64_t)NB);
+                const double2 a = c.twa[t * (NB + 1) + j];
+                v[0] = cmul(v[0], a);
 #pragma unroll
-                for (int r = 0; r < RS; ++r) v[r] = cmul(v[r], q[r]);
+                for (int r = 1; r < RS; ++r) v[r] = cmul(v[r], cmul(a, c.twb[t * (RS + 1) + r]));
             }
+            if (d.pack_lp >= 0) {   // general pack (single-level local transform, p > 1)
 #pragma unroll
-            for (int r = 0; r < RS; ++r) {
-                int64_t k = j + r * NB;
-                double2 val = v[r];
-                if (d.conj_out) val.y = -val.y;
-                int64_t addr;
-                if (d.last) {
-                    int64_t K = k_base + (int64_t)t * d.K_t + k * d.K_k;
-                    addr = d.pack_lp >= 0
-                               ? (K & ((1ll << d.pack_lp) - 1)) * d.pack_chunk + (K >> d.pack_lp)
-                               : K;
-                } else {
-                    addr = in_base - io.out_shift + (int64_t)t * d.in_t + k * d.in_f;
+                for (int r = 0; r < RS; ++r) {
+                    const int64_t K = c.k_base + (int64_t)t * d.K_t + (int64_t)(j + r * NB) * d.K_k;
+                    const int64_t addr = (K & ((1ll << d.pack_lp) - 1)) * d.pack_chunk + (K >> d.pack_lp);
+                    st_io<ST>(c.out + addr, conj_mask(v[r], cm), pol);
                 }
-                st_io<ST>(io.dst + addr, val, pol);
+            } else {
+                double2 *po = c.out + (int64_t)t * d.out_t + (int64_t)j * d.out_k;
+#pragma unroll
+                for (int r = 0; r < RS; ++r) st_io<ST>(po + r * so, conj_mask(v[r], cm), pol);
             }
         }
     }
 }
 
 template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
-__device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileIO &io,
-                                           const double2 *inbuf, const Hook &hook, int64_t in_base,
-                                           int64_t k_base, uint64_t al_base, uint64_t be_base) {
+__device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
+                                           const double2 *inbuf, const Hook &hook) {
     constexpr int REM = F / NS;
     constexpr int RS = REM >= 16 ? 16 : REM;
-    fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base, be_base);
-    if constexpr (NS * RS < F)
-        fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base,
-                                                    be_base);
+    fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
+    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
 }
 
 // one tile of T transforms; tile id -> (u, v, w) as documented in PassDesc
 template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
-__device__ __forceinline__ void tile_fft(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b,
+__device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDesc &d, const TileIO &io, int64_t b,
                                          const double2 *inbuf = nullptr, const Hook &hook = Hook()) {
     const int64_t u = b % d.U;
     b /= d.U;
     const int64_t v = b % d.V;
     const int64_t w = b / d.V;
-    const int64_t in_base = u * d.in_u + v * d.in_v + w * d.in_w;
-    const int64_t k_base = u * d.K_u + v * d.K_v + w * d.K_w;
-    const uint64_t al_base = (uint64_t)d.a_c + (uint64_t)u * d.a_u + (uint64_t)v * d.a_v + (uint64_t)w * d.a_w;
-    const uint64_t be_base = (uint64_t)d.b_c + (uint64_t)u * d.b_u + (uint64_t)v * d.b_v + (uint64_t)w * d.b_w;
+    TileCtx c;
+    c.in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
+    c.out = io.dst + (u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
+    c.k_base = u * d.K_u + v * d.K_v + w * d.K_w;
+    c.al = (uint32_t)d.a_c + (uint32_t)u * (uint32_t)d.a_u + (uint32_t)v * (uint32_t)d.a_v + (uint32_t)w * (uint32_t)d.a_w;
+    c.be = (uint32_t)d.b_c + (uint32_t)u * (uint32_t)d.b_u + (uint32_t)v * (uint32_t)d.b_v + (uint32_t)w * (uint32_t)d.b_w;
+    using SH = PassShape<F, T>;
+    double2 *twa = tw;
+    double2 *twb = twa + SH::TWA / sizeof(double2);
+    c.twa = twa;
+    c.twb = twb;
     double2 x[PassShape<F, T>::R];
-    fft_stages<F, T, 1, SRC, Hook, LD, ST>(x, sm, d, io, inbuf, hook, in_base, k_base, al_base, be_base);
+    fft_stages<F, T, 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
 }
 
 template <int F, int T>
@@ -360,7 +456,8 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     fft_pass_kernel(const PassDesc d) {
     extern __shared__ double2 sm[];
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
-    tile_fft<F, T>(sm, d, io, blockIdx.x);
+    tile_fft<F, T>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
+                   blockIdx.x);
 }
 
 template <int F, int T>
@@ -395,7 +492,10 @@ struct TmaShape {
     static constexpr int NBOX = F / FB;
     static constexpr unsigned BOX_BYTES = (unsigned)(FB * T * 16);
     static constexpr size_t IN_BYTES = (size_t)T * F * 16;
-    static constexpr size_t SMEM = 128 + IN_BYTES + PassShape<F, T>::SMEM + 16;
+    // one buffer = the TMA staging tile, reused in place as the exchange buffer
+    static constexpr size_t BUF = ((IN_BYTES > PassShape<F, T>::XCH ? IN_BYTES : PassShape<F, T>::XCH) + 127) / 128 * 128;
+    static constexpr size_t TW = PassShape<F, T>::TWA + PassShape<F, T>::TWB;
+    static constexpr size_t SMEM = 128 + 2 * BUF + TW + 32;
 };
 
 template <int F, int T, int SRC>
@@ -417,35 +517,45 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap *map, uint64_t 
     }
 }
 
+struct SyncHook {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+#ifndef MOA_TMA_MINB
+#define MOA_TMA_MINB 3
+#endif
+// Persistent TMA pass, double buffered: while tile i is transformed in buffer
+// i&1 (staged input, then reused in place for the exchanges), the copy of tile
+// i+1 streams into the other buffer.
 template <int F, int T, int SRC>
-__global__ void __launch_bounds__(PassShape<F, T>::NT, 1)
+__global__ void __launch_bounds__(PassShape<F, T>::NT, (T * F <= 2048) ? MOA_TMA_MINB : 1)
     fft_pass_tma_kernel(const PassDesc d, const __grid_constant__ CUtensorMap tmap, int64_t tiles) {
+    using TS = TmaShape<F, T, SRC>;
     extern __shared__ unsigned char smraw[];
-    double2 *inbuf = reinterpret_cast<double2 *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
-    double2 *work = inbuf + T * F;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(work + (PassShape<F, T>::SMEM / sizeof(double2)));
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    double2 *buf[2] = {reinterpret_cast<double2 *>(base), reinterpret_cast<double2 *>(base + TS::BUF)};
+    double2 *tw = reinterpret_cast<double2 *>(base + 2 * TS::BUF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + 2 * TS::BUF + TS::TW);
     const int tid = threadIdx.x;
     if (tid == 0) {
-        mbar_init(bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
     int64_t tile = blockIdx.x;
-    if (tid == 0 && tile < tiles) tma_issue_tile<F, T, SRC>(&tmap, bar, inbuf, d, tile);
+    if (tid == 0 && tile < tiles) tma_issue_tile<F, T, SRC>(&tmap, &bar[0], buf[0], d, tile);
     const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
-    unsigned phase = 0;
-    for (; tile < tiles; tile += gridDim.x) {
-        mbar_wait(bar, phase);
-        phase ^= 1;
+    for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
+        const int b = it & 1;
+        __syncthreads();   // the previous tile is done with buf[b^1] and the twiddle tables
         const int64_t next = tile + gridDim.x;
-        auto hook = [&]() {
-            __syncthreads();   // every lane has its inputs in registers: the staging buffer is free
-            if (tid == 0 && next < tiles) {
-                fence_proxy_async();
-                tma_issue_tile<F, T, SRC>(&tmap, bar, inbuf, d, next);
-            }
-        };
-        tile_fft<F, T, SRC>(work, d, io, tile, inbuf, hook);
+        if (tid == 0 && next < tiles) {
+            fence_proxy_async();
+            tma_issue_tile<F, T, SRC>(&tmap, &bar[b ^ 1], buf[b ^ 1], d, next);
+        }
+        mbar_wait(&bar[b], (it >> 1) & 1);
+        tile_fft<F, T, SRC, SyncHook>(buf[b], tw, d, io, tile, buf[b], SyncHook());
     }
 }
 

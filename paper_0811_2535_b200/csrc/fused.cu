@@ -41,60 +41,122 @@ template <int F2, int T2, int F3, int T3>
 struct FusedShape {
     static constexpr int NT = PassShape<F2, T2>::NT;
     static_assert(PassShape<F3, T3>::NT == NT, "fused passes need equal block sizes");
-    static constexpr size_t SMEM =
-        PassShape<F2, T2>::SMEM > PassShape<F3, T3>::SMEM ? PassShape<F2, T2>::SMEM : PassShape<F3, T3>::SMEM;
-    static constexpr int MINB = PassShape<F2, T2>::MINB;
+    using S2 = TmaShape<F2, T2, 1>;
+    using S3 = TmaShape<F3, T3, 2>;
+    static constexpr size_t BUF = S2::BUF > S3::BUF ? S2::BUF : S3::BUF;
+    static constexpr size_t TW = S2::TW > S3::TW ? S2::TW : S3::TW;
+    static constexpr size_t SMEM = 128 + 2 * BUF + TW + 64;
+    static constexpr int MINB = (T2 * F2 <= 2048) ? 3 : 1;
 };
 
+// row tile of the scratch ring: dims {2F3 doubles, T3 rows (stride F2F3), F2 (stride F3), slots}
+template <int F3, int T3>
+__device__ __forceinline__ void tma_issue_scratch(const CUtensorMap *map, uint64_t *bar, double2 *dst, int tile,
+                                                  int slot) {
+    using S3 = TmaShape<F3, T3, 2>;
+    mbar_expect_tx(bar, S3::BOX_BYTES * S3::NBOX);
+#pragma unroll
+    for (int k = 0; k < S3::NBOX; ++k) tma_load_4d(dst + k * S3::FB * T3, map, bar, 2 * S3::FB * k, 0, tile, slot);
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Persistent, double-buffered: while item i is transformed in buffer i&1 the
+// next item has already been claimed and (when its inputs are ready) its tile
+// is streaming into the other buffer by TMA -- from HBM for a middle-pass item,
+// from the L2-resident scratch ring for a last-pass item.
 template <int F2, int T2, int F3, int T3>
 __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2, T2, F3, T3>::MINB)
-    fused_kernel(const FusedDesc fd) {
-    extern __shared__ double2 sm[];
-    __shared__ long long s_item;
+    fused_kernel(const FusedDesc fd, const __grid_constant__ CUtensorMap map2, const __grid_constant__ CUtensorMap map3) {
+    using SH = FusedShape<F2, T2, F3, T3>;
+    extern __shared__ unsigned char smraw[];
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    double2 *buf[2] = {reinterpret_cast<double2 *>(base), reinterpret_cast<double2 *>(base + SH::BUF)};
+    double2 *tw = reinterpret_cast<double2 *>(base + 2 * SH::BUF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + 2 * SH::BUF + SH::TW);
+    __shared__ long long s_item[2];
+    __shared__ int s_issued[2];
+    const int tid = threadIdx.x;
     const unsigned long long claim_base = fd.epoch * (unsigned long long)(fd.total_items + gridDim.x);
     const unsigned long long tgt2 = (fd.epoch + 1) * (unsigned long long)fd.tiles2;
     const unsigned long long tgt3 = (fd.epoch + 1) * (unsigned long long)fd.tiles3;
-    for (;;) {
-        __syncthreads();   // the previous tile's shared-memory reads are done
-        if (threadIdx.x == 0) s_item = (long long)(atomicAdd(fd.claim, 1ull) - claim_base);
-        __syncthreads();
-        const long long item = s_item;
+
+    // thread 0: start the copy of `item` into buffer b (wait for its inputs only if `block`)
+    auto try_issue = [&](long long item, int b, bool block) -> bool {
+        const int code = __ldg(fd.items + item);
+        const int kind = code >> 30, g = (code >> 16) & 0x3fff, tile = code & 0xffff;
+        if (kind == 1) {
+            if (ld_acquire_u64(fd.done2 + g) < tgt2) {
+                if (!block) return false;
+                wait_geq(fd.done2 + g, tgt2);
+            }
+            fence_proxy_async_global();   // the generic-proxy scratch writes are visible to TMA
+            fence_proxy_async();
+            tma_issue_scratch<F3, T3>(&map3, &bar[b], buf[b], tile, g % fd.slots);
+        } else {
+            fence_proxy_async();
+            tma_issue_tile<F2, T2, 1>(&map2, &bar[b], buf[b], fd.p2, (int64_t)g * fd.tiles2 + tile);
+        }
+        return true;
+    };
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        const long long first = (long long)(atomicAdd(fd.claim, 1ull) - claim_base);
+        s_item[0] = first;
+        s_issued[0] = 1;
+        if (first < fd.total_items) try_issue(first, 0, true);
+    }
+    unsigned uses[2] = {0, 0};
+    for (int it = 0;; ++it) {
+        const int b = it & 1;
+        __syncthreads();   // previous item finished (buffer b^1, twiddle tables free)
+        const long long item = s_item[b];
         if (item >= fd.total_items) break;
         const int code = __ldg(fd.items + item);
         const int kind = code >> 30, g = (code >> 16) & 0x3fff, tile = code & 0xffff;
+        if (tid == 0) {
+            // claim the next item and prefetch it into the other buffer if its inputs are ready
+            const long long nxt = (long long)(atomicAdd(fd.claim, 1ull) - claim_base);
+            s_item[b ^ 1] = nxt;
+            s_issued[b ^ 1] = (nxt < fd.total_items) ? (int)try_issue(nxt, b ^ 1, false) : 1;
+            if (kind == 0 && g >= fd.slots) wait_geq(fd.done3 + (g - fd.slots), tgt3);   // slot free
+            if (!s_issued[b]) try_issue(item, b, true);
+        }
+        __syncthreads();
+        mbar_wait(&bar[b], uses[b] & 1);
+        uses[b]++;
         const int slot = g % fd.slots;
         double2 *slot_ptr = fd.scratch + (int64_t)slot * fd.rows_per_group_elems;
         const int64_t shift = (int64_t)g * fd.rows_per_group_elems;
         if (kind == 0) {
-            if (g >= fd.slots) {
-                if (threadIdx.x == 0) wait_geq(fd.done3 + (g - fd.slots), tgt3);
-                __syncthreads();
-            }
             TileIO io{fd.work, slot_ptr, 0, shift};
-            tile_fft<F2, T2, 0, NoHook, 0, 0>(sm, fd.p2, io, (int64_t)g * fd.tiles2 + tile);
+            tile_fft<F2, T2, 1, SyncHook, 0, 0>(buf[b], tw, fd.p2, io, (int64_t)g * fd.tiles2 + tile, buf[b],
+                                               SyncHook());
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 __threadfence();
                 atomicAdd(fd.done2 + g, 1ull);
             }
         } else {
-            if (threadIdx.x == 0) wait_geq(fd.done2 + g, tgt2);
-            __syncthreads();
-            TileIO io{slot_ptr, fd.out, shift, 0};
-            tile_fft<F3, T3, 0, NoHook, 1, 1>(sm, fd.p3, io, (int64_t)g + (int64_t)(fd.groups) * tile);
-            __syncthreads();
             if (fd.discard) {
-                // the consumed scratch lines are dead: drop them from L2 without write-back.
-                // This tile read T3 segments of F3 elements at slot offsets tile*F3 + t*F2*F3.
+                // the staged scratch lines are dead: drop them from L2 without write-back
                 constexpr int LINES_PER_SEG = F3 * 16 / 128;
-                for (int i = threadIdx.x; i < T3 * LINES_PER_SEG; i += blockDim.x) {
-                    int t = i / LINES_PER_SEG, l = i % LINES_PER_SEG;
+                for (int i = tid; i < T3 * LINES_PER_SEG; i += SH::NT) {
+                    const int t = i / LINES_PER_SEG, l = i % LINES_PER_SEG;
                     const double2 *a = slot_ptr + (int64_t)tile * F3 + (int64_t)t * fd.f2f3 + l * 8;
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
                 }
-                __syncthreads();
             }
-            if (threadIdx.x == 0) {
+            TileIO io{slot_ptr, fd.out, shift, 0};
+            tile_fft<F3, T3, 2, SyncHook, 0, 1>(buf[b], tw, fd.p3, io, (int64_t)g + (int64_t)fd.groups * tile,
+                                               buf[b], SyncHook());
+            __syncthreads();
+            if (tid == 0) {
                 __threadfence();
                 atomicAdd(fd.done3 + g, 1ull);
             }
@@ -103,7 +165,8 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
 }
 
 template <int F2, int T2, int F3, int T3>
-static cudaError_t launch_f(const FusedDesc &fd, int grid, cudaStream_t s) {
+static cudaError_t launch_f(const FusedDesc &fd, const CUtensorMap &m2, const CUtensorMap &m3, int grid,
+                            cudaStream_t s) {
     using SH = FusedShape<F2, T2, F3, T3>;
     static bool attr = false;
     if (!attr) {
@@ -114,7 +177,7 @@ static cudaError_t launch_f(const FusedDesc &fd, int grid, cudaStream_t s) {
         }
         attr = true;
     }
-    fused_kernel<F2, T2, F3, T3><<<grid, SH::NT, SH::SMEM, s>>>(fd);
+    fused_kernel<F2, T2, F3, T3><<<grid, SH::NT, SH::SMEM, s>>>(fd, m2, m3);
     return cudaGetLastError();
 }
 
@@ -144,7 +207,6 @@ static int grid_f() {
     X(8, 16, 9, 8)        \
     X(9, 8, 8, 16)        \
     X(10, 4, 10, 4)       \
-    X(10, 8, 10, 8)       \
     X(7, 32, 8, 16)
 
 int fused_supported(int logF2, int T2, int logF3, int T3) {
@@ -155,9 +217,10 @@ int fused_supported(int logF2, int T2, int logF3, int T3) {
     return 0;
 }
 
-cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, int grid, cudaStream_t s) {
+cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, const CUtensorMap &m2,
+                         const CUtensorMap &m3, int grid, cudaStream_t s) {
 #define X(a, b, c, d) \
-    if (logF2 == a && T2 == b && logF3 == c && T3 == d) return launch_f<1 << a, b, 1 << c, d>(fd, grid, s);
+    if (logF2 == a && T2 == b && logF3 == c && T3 == d) return launch_f<1 << a, b, 1 << c, d>(fd, m2, m3, grid, s);
     MOA_FUSED_LIST(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -30,6 +30,9 @@ struct PassDesc {
     int64_t in_u, in_v, in_w, in_t, in_f;
     // last pass: output index K = K_u*u + K_v*v + K_w*w + K_t*t + K_k*k
     int64_t K_u, K_v, K_w, K_t, K_k;
+    // output address of point k of transform t: out_u*u + out_v*v + out_w*w + out_t*t + out_k*k
+    // (= the input map for in-place middle passes, K for the last pass, K's send slot when packing)
+    int64_t out_u, out_v, out_w, out_t, out_k;
     // twiddle exponent e = alpha + beta*k (mod n),
     //   alpha = a_u*u + a_v*v + a_w*w + a_t*t,  beta = b_u*u + b_v*v + b_w*w + b_t*t
     //   (+ the constants a_c, b_c)
@@ -37,11 +40,13 @@ struct PassDesc {
     int64_t b_c, b_u, b_v, b_w, b_t;
     uint64_t nmask;         // n - 1 (the GLOBAL n of the transform)
     int hbits;              // split of the two-level table
+    int tbits;              // log2 n
     int last;               // 1: store to K (or its pack); 0: store in place at (t, k) of the input view
     int twiddle;            // 1: multiply by omega_n^e before the store
     int conj_in, conj_out;  // sign +1 is computed as conj(FFT_-1(conj x))
     int in_tfast, out_tfast;// lane->(t, j) order of the global-facing stages
-    int pack_lp;            // >= 0: send layout addr = (K & (P-1)) * pack_chunk + (K >> pack_lp)
+    int pack_lp;            // >= 0: general send layout addr = (K & (P-1)) * pack_chunk + (K >> pack_lp)
+                            //       (only for a single-level local transform; else out_* is affine)
     int64_t pack_chunk;
     int64_t in_shift;       // subtracted from every input address (src is a window of the view)
     int64_t out_shift;      // subtracted from every in-place output address (dst is a window)
@@ -79,7 +84,8 @@ int pass_tma_grid(int logF, int T, int src);
 cudaError_t launch_pass_tma(int logF, int T, int src, const PassDesc &d, const CUtensorMap &map, int64_t tiles,
                             int grid, cudaStream_t s);
 int fused_supported(int logF2, int T2, int logF3, int T3);
-cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, int grid, cudaStream_t s);
+cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, const CUtensorMap &m2,
+                         const CUtensorMap &m3, int grid, cudaStream_t s);
 int fused_grid(int logF2, int T2, int logF3, int T3);
 
 cudaError_t launch_bitrev(const double2 *in, double2 *out, int t, int conj_in, cudaStream_t s);

@@ -190,6 +190,7 @@ struct moa_fft_plan_s {
     // L2-fused last two passes (fused.cu)
     bool fused = false;
     FusedDesc fd;
+    CUtensorMap fmap2, fmap3;
     int fgrid = 0;
     int *items = nullptr;
     unsigned long long *counters = nullptr;
@@ -290,6 +291,7 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
         pp.logF = ilog2(F);
         D.nmask = (uint64_t)n - 1;
         D.hbits = pl->hbits;
+        D.tbits = pl->t;
         D.tw_hi = pl->tw_hi;
         D.tw_lo = pl->tw_lo;
         D.tw_f = pl->tw_f;
@@ -314,6 +316,11 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
             D.in_tfast = T > 1;
             D.out_tfast = T > 1;
             D.last = 0;
+            D.out_u = D.in_u;
+            D.out_v = D.in_v;
+            D.out_w = D.in_w;
+            D.out_t = D.in_t;
+            D.out_k = D.in_f;
             pp.tiles = D.U * D.V;
         } else {
             // last pass: rows of length F indexed by the digits (k_0 .. k_{d-2}) the
@@ -391,6 +398,22 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
                 D.b_c = (int64_t)(r * (uint64_t)D.K_k);
             }
             D.conj_out = (P == 1 && pl->sign > 0);
+            if (P == 1) {
+                D.out_u = D.K_u;
+                D.out_v = D.K_v;
+                D.out_w = D.K_w;
+                D.out_t = D.K_t;
+                D.out_k = D.K_k;
+            } else if (d > 1) {
+                // send slot of K = dst + P*c is dst*chunk + K/P; with the tile rows
+                // k_0 = dst + P*(u*T + t) every coefficient but v's is a multiple of P
+                D.pack_lp = -1;
+                D.out_u = D.K_u / P;
+                D.out_v = pl->M / P;
+                D.out_w = D.K_w / P;
+                D.out_t = D.K_t / P;
+                D.out_k = D.K_k / P;
+            }
         }
         if (!pass_supported(pp.logF, pp.T))
             return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
@@ -475,6 +498,22 @@ static int setup_fused(moa_fft_plan_s *pl) {
     fd.scratch = pl->scratch;
     fd.f2f3 = F2 * F3;
     fd.discard = env_int("MOA_FFT_DISCARD", 1);
+    {   // TMA maps: middle-pass column tiles over `work`, last-pass row tiles over the ring
+        PassPlan tmp = p2;
+        tmp.tma = 1;
+        int rc = encode_pass_map(tmp, pl->work);
+        if (rc) return rc;
+        pl->fmap2 = tmp.map;
+        EncodeTiledFn enc = encode_fn();
+        cuuint64_t dims[4] = {(cuuint64_t)(2 * F3), (cuuint64_t)T3, (cuuint64_t)F2, (cuuint64_t)slots};
+        cuuint64_t strides[3] = {(cuuint64_t)(16 * F2 * F3), (cuuint64_t)(16 * F3), (cuuint64_t)(16 * group_elems)};
+        cuuint32_t box[4] = {(cuuint32_t)(F3 < 128 ? 2 * F3 : 256), (cuuint32_t)T3, 1, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = enc(&pl->fmap3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, pl->scratch, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MOA_ERR_CUDA, "scratch tensor map encode failed (%d)", (int)r);
+    }
     pl->fgrid = fused_grid(p2.logF, p2.T, p3.logF, p3.T);
     int gmax = env_int("MOA_FFT_FGRID", 0);
     if (gmax > 0 && gmax < pl->fgrid) pl->fgrid = gmax;
@@ -513,8 +552,8 @@ static int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt) {
 static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_plan_s **res) {
     *res = nullptr;
     int mode = opt ? opt->mode : MOA_MODE_LIFTED;
-    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 34))
-        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 34 (Fig 2.1: n = 2^t, t >= 1)",
+    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 32))
+        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 32 (Fig 2.1: n = 2^t, t >= 1)",
                     (long long)n);
     if (sign != -1 && sign != 1) return fail(MOA_ERR_INVALID_SIGN, "sign=%d must be -1 or +1", sign);
     if (mode < MOA_MODE_LIFTED || mode > MOA_MODE_EMULATED)
@@ -725,7 +764,7 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
                  pl->passes[1].T, 1 << pl->passes[2].logF, pl->passes[2].T);
         ProfScope sc(pl, name, 32 * pl->M);
         CUDA_TRY(launch_fused(pl->passes[1].logF, pl->passes[1].T, pl->passes[2].logF, pl->passes[2].T, fd,
-                              pl->fgrid, s));
+                              pl->fmap2, pl->fmap3, pl->fgrid, s));
         return MOA_OK;
     }
     if (pl->p == 1) return run_passes(pl, pl->passes, in, out);
@@ -850,8 +889,8 @@ const char *moa_fft_last_error(void) { return g_err.c_str(); }
 
 int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opts, int pass, int64_t *in_idx,
                           int64_t *out_idx, int64_t *tw_exp, int64_t *F_out) {
-    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 34))
-        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 34", (long long)n);
+    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 32))
+        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 32", (long long)n);
     if (!pow2(p) || p > 16 || n / p < p)
         return fail(MOA_ERR_INVALID_P, "p=%d invalid for n=%lld (power of two, psize >= m, P:289)", p,
                     (long long)n);
@@ -887,11 +926,11 @@ int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opt
                 if (i >= tmp.M) return fail(MOA_ERR_INVALID_ARG, "internal: pass covers more than n/p");
                 in_idx[i] = in_base + t * D.in_t + f * D.in_f;
                 int64_t o;
-                if (D.last) {
+                if (D.last && D.pack_lp >= 0) {
                     int64_t K = k_base + t * D.K_t + f * D.K_k;
-                    o = D.pack_lp >= 0 ? (K & (((int64_t)1 << D.pack_lp) - 1)) * D.pack_chunk + (K >> D.pack_lp) : K;
+                    o = (K & (((int64_t)1 << D.pack_lp) - 1)) * D.pack_chunk + (K >> D.pack_lp);
                 } else {
-                    o = in_base + t * D.in_t + f * D.in_f;
+                    o = u * D.out_u + v * D.out_v + w * D.out_w + t * D.out_t + f * D.out_k;
                 }
                 out_idx[i] = o;
                 tw_exp[i] = D.twiddle ? (int64_t)((al + t * (uint64_t)D.a_t + (be + t * (uint64_t)D.b_t) * (uint64_t)f) &

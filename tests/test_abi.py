@@ -49,7 +49,7 @@ def test_library_is_sm100a_cubin():
     (6, 1, -1, -1, "2^t"),
     (1, 1, -1, -1, "2^t"),
     (0, 1, -1, -1, "2^t"),
-    (1 << 35, 1, -1, -1, "t <= 34"),
+    (1 << 33, 1, -1, -1, "t <= 32"),
     (16, 1, 0, -3, "sign"),
     (16, 3, -1, -2, "power of two"),
     (16, 8, -1, -2, "psize >= m"),     # n=16, m=8 rejected
