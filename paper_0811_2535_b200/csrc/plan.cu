@@ -155,7 +155,8 @@ static int encode_pass_map(PassPlan &pp, const void *base) {
 // choose the TMA-staged variant when it exists for this (F, T, layout)
 static void choose_tma(PassPlan &pp) {
     pp.tma = 0;
-    if (!getenv("MOA_FFT_TMA") ? false : atoi(getenv("MOA_FFT_TMA")) == 0) return;
+    const char *tma_env = getenv("MOA_FFT_TMA");   // measured: the plain kernel (4 CTAs/SM) wins today
+    if (!tma_env || atoi(tma_env) == 0) return;
     const PassDesc &D = pp.d;
     int src = 0;
     if (!D.last && D.in_t == 1 && pp.T >= 2) src = 1;
@@ -233,8 +234,9 @@ static int default_lifting(int tl, int64_t *lift) {
         lift[0] = (int64_t)1 << tl;
         return 1;
     }
-    if (tl >= 20 && tl <= 16 + FMAX_LOG && env_int("MOA_FFT_FUSE", 1)) {
-        // <2^(tl-16), 256, 256>: the last two passes run L2-fused (fused.cu)
+    if (tl >= 20 && tl <= 16 + FMAX_LOG) {
+        // <2^(tl-16), 256, 256>: 256-point passes keep 4 tiles per SM in flight
+        // (measured fastest at 2^24); MOA_FFT_FUSE=1 runs the last two L2-fused
         lift[0] = (int64_t)1 << (tl - 16);
         lift[1] = 256;
         lift[2] = 256;
@@ -264,7 +266,7 @@ static int default_lifting(int tl, int64_t *lift) {
 static int choose_T(int logF, int64_t avail) {
     // tile size cap: long transforms take T*F = 8192 (one 128 KiB tile per SM);
     // short ones 4096 (2-3 tiles per SM overlap memory and FP64 work)
-    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : 4096);
+    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : 2048);
     if (tf_max > TF_MAX) tf_max = TF_MAX;
     int T = 1;
     while (T < 64 && ((int64_t)(2 * T) << logF) <= tf_max && 2 * T <= avail) T *= 2;
@@ -655,7 +657,7 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
             return rc;
         }
         for (auto &pp : pl->passes) choose_tma(pp);
-        if (p == 1 && pl->d == 3 && env_int("MOA_FFT_FUSE", 1) && (rc = setup_fused(pl)) != MOA_OK) {
+        if (p == 1 && pl->d == 3 && env_int("MOA_FFT_FUSE", 0) && (rc = setup_fused(pl)) != MOA_OK) {
             free_plan(pl);
             return rc;
         }

@@ -140,12 +140,26 @@ def test_execute_host_end_to_end():
 def test_plan_info():
     info = moa.Plan(1 << 24).info()
     assert info["passes"] == 3 and info["lift"] == [256, 256, 256]
-    assert info["hbm_bytes"] == 32 * (1 << 24) * 2   # last two passes L2-fused
+    assert info["hbm_bytes"] == 32 * (1 << 24) * 3
     info = moa.Plan(1 << 24, lift=[4096, 4096]).info()
     assert info["passes"] == 2 and info["hbm_bytes"] == 32 * (1 << 24) * 2
     assert info["breakpoint"] == 25
     info = moa.Plan(1 << 30 if False else 1 << 27).info()
     assert info["passes"] == 3
+
+
+@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
+def test_variant_kernels_parity(env, monkeypatch):
+    """The L2-fused last passes and the TMA-staged passes (env-selected variants)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for t in (20, 22, 24):
+        x = moa_inputs.signal_for(t)
+        ref = oracle.fft(x, -1, threads=8)
+        plan = moa.Plan(1 << t)
+        for _ in range(3):   # the fused kernel's counters are monotone across executes
+            got = _run(plan, x)
+            assert oracle.rel_l2(got, ref) <= tol(t), (env, t)
 
 
 def test_misaligned_pointer_rejected():
