@@ -15,7 +15,7 @@ a = ap.parse_args()
 raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
-names = [n for n in a.names.split(",") if n]
+names = [n for n in a.names.split(";") if n]
 def g(r, k):
     return r[hdr.index(k)] if k in hdr else ""
 lines = [f"# ncu summary: {os.path.basename(a.rep)}", "",
