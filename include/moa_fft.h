@@ -119,6 +119,19 @@ int moa_fft_execute(moa_fft_plan_t plan, const void *in, void *out);
  */
 int moa_fft_execute_host(moa_fft_plan_t plan, const void *host_in, void *host_out);
 
+/*
+ * Pipelined end-to-end form for a stream of `count` independent transforms:
+ * host_in[i] -> host_out[i] (HOST pointers, pinned for full speed, same layout
+ * as moa_fft_execute_host).  Two device staging pairs and two copy streams let
+ * the host->device copy of transform i+1 and the device->host copy of
+ * transform i-1 overlap the execute of transform i (PCIe is full duplex).
+ * Synchronises before returning; every host_out[i] is then complete.
+ * Returns MOA_OK, MOA_ERR_INVALID_ARG (NULL plan, count < 0), MOA_ERR_ALIGN (a
+ * NULL buffer), MOA_ERR_OOM, or the first execute / CUDA error.
+ */
+int moa_fft_execute_host_batch(moa_fft_plan_t plan, int count, const void *const *host_in,
+                               void *const *host_out);
+
 /* Free everything the plan owns (synchronises its stream first).  NULL-safe. */
 void moa_fft_destroy(moa_fft_plan_t plan);
 

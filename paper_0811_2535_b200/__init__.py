@@ -36,6 +36,11 @@ class _Options(ctypes.Structure):
                 ("chunks", ctypes.c_int)]
 
 
+class _KernelStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 64), ("launches", ctypes.c_int), ("total_ms", ctypes.c_double),
+                ("alg_bytes", ctypes.c_int64)]
+
+
 class _Info(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("t", ctypes.c_int), ("p", ctypes.c_int), ("rank", ctypes.c_int),
                 ("sign", ctypes.c_int), ("mode", ctypes.c_int), ("local_n", ctypes.c_int64),
@@ -44,7 +49,7 @@ class _Info(ctypes.Structure):
                 ("hbm_bytes", ctypes.c_int64), ("a2a_bytes", ctypes.c_int64)]
 
 
-EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host",
+EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host", "moa_fft_execute_host_batch",
            "moa_fft_destroy", "moa_fft_set_stream", "moa_fft_plan_info", "moa_fft_last_error",
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass"]
@@ -73,6 +78,7 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_plan_ex.restype = vp
     lib.moa_fft_execute.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
+    lib.moa_fft_execute_host_batch.argtypes = [vp, ci, vp, vp]
     lib.moa_fft_destroy.argtypes = [vp]
     lib.moa_fft_destroy.restype = None
     lib.moa_fft_set_stream.argtypes = [vp, vp]
@@ -171,6 +177,35 @@ class Plan:
         if rc:
             _err(rc)
         return host_out
+
+    def execute_host_batch(self, host_ins, host_outs):
+        """Pipelined end-to-end: transform host_ins[i] into host_outs[i] (pinned host
+        tensors), copies overlapping the transforms; synchronises."""
+        k = len(host_ins)
+        if len(host_outs) != k:
+            raise ValueError("host_ins and host_outs differ in length")
+        ins = (ctypes.c_void_p * max(k, 1))(*[_ptr(h) for h in host_ins])
+        outs = (ctypes.c_void_p * max(k, 1))(*[_ptr(h) for h in host_outs])
+        rc = _lib.moa_fft_execute_host_batch(self._h, k, ins, outs)
+        if rc:
+            _err(rc)
+        return host_outs
+
+    def set_profiling(self, enable: bool = True):
+        """Bracket every kernel launch with CUDA events (moa_fft_set_profiling)."""
+        rc = _lib.moa_fft_set_profiling(self._h, 1 if enable else 0)
+        if rc:
+            _err(rc)
+
+    def get_profile(self) -> list:
+        """Per-kernel event times since the last call (moa_fft_get_profile); resets them."""
+        buf = (_KernelStat * 32)()
+        k = _lib.moa_fft_get_profile(self._h, buf, 32)
+        if k < 0:
+            _err(k)
+        return [{"name": buf[i].name.decode(), "launches": buf[i].launches,
+                 "avg_us": buf[i].total_ms * 1e3 / max(1, buf[i].launches),
+                 "alg_bytes": int(buf[i].alg_bytes)} for i in range(k)]
 
     def destroy(self):
         if getattr(self, "_h", None):

@@ -86,6 +86,18 @@ __device__ __forceinline__ void dft_reg(double2 *v) {
     for (int k = 0; k < R; ++k) v[k] = tmp[k];
 }
 
+// p + off elements with a 32-bit element offset: one IMAD.WIDE.U32 per address
+// (the byte offset itself may exceed 32 bits)
+template <class Tp>
+__device__ __forceinline__ Tp *elem_off(Tp *p, uint32_t off) {
+    return reinterpret_cast<Tp *>(reinterpret_cast<uintptr_t>(p) + (uint64_t)off * 16u);
+}
+// p + c * stride elements, c a compile-time constant
+template <class Tp>
+__device__ __forceinline__ Tp *elem_off_c(Tp *p, uint32_t c, uint32_t stride) {
+    return reinterpret_cast<Tp *>(reinterpret_cast<uintptr_t>(p) + (uint64_t)(16u * c) * (uint64_t)stride);
+}
+
 // omega_n^e from the two-level table: hi[e >> h] * lo[e & (2^h - 1)]
 __device__ __forceinline__ double2 tw2(const double2 *__restrict__ hi, const double2 *__restrict__ lo,
                                        uint32_t e, int h) {
@@ -115,26 +127,36 @@ __device__ __forceinline__ void twiddle_run(double2 *q, const PassDesc &d, uint3
     for (int r = 8; r < RS; ++r) q[r] = cmul(q[r - 8], p8);
 }
 
-// stage twiddles omega_{NsR}^(r*k) = omega_FMAX^(r*e1), e1 = k*FMAX/(Ns*RS): 4 loads + products
+// stage twiddles omega_{Ns*RS}^(r*k) = omega_FMAX^(r*e1), e1 = k*FMAX/(Ns*RS).
+//   MOA_STW_LOAD 1: one L1-resident table load per point (no products);
+//   MOA_STW_LOAD 0: 4 table loads (r = 1, 2, 4, 8) and products for the rest
+//                   (fewer loads on the latency-critical path between the stages)
+#ifndef MOA_STW_LOAD
+#define MOA_STW_LOAD 0
+#endif
 template <int RS>
 __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restrict__ tf, int e1) {
     if (RS == 1 || e1 == 0) return;
+#if MOA_STW_LOAD
+#pragma unroll
+    for (int r = 1; r < RS; ++r) x[r] = cmul(x[r], __ldg(tf + r * e1));
+#else
     double2 w1 = __ldg(tf + e1);
+    double2 w2 = RS > 2 ? __ldg(tf + 2 * e1) : w1;
+    double2 w4 = RS > 4 ? __ldg(tf + 4 * e1) : w1;
+    double2 w8 = RS > 8 ? __ldg(tf + 8 * e1) : w1;
     x[1] = cmul(x[1], w1);
     if (RS == 2) return;
-    double2 w2 = __ldg(tf + 2 * e1);
     double2 w3 = cmul(w1, w2);
     x[2] = cmul(x[2], w2);
     x[3] = cmul(x[3], w3);
     if (RS == 4) return;
-    double2 w4 = __ldg(tf + 4 * e1);
     double2 w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
     x[4] = cmul(x[4], w4);
     x[5] = cmul(x[5], w5);
     x[6] = cmul(x[6], w6);
     x[7] = cmul(x[7], w7);
     if (RS == 8) return;
-    double2 w8 = __ldg(tf + 8 * e1);
     x[8] = cmul(x[8], w8);
     x[9] = cmul(x[9], cmul(w1, w8));
     x[10] = cmul(x[10], cmul(w2, w8));
@@ -143,6 +165,7 @@ __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restr
     x[13] = cmul(x[13], cmul(w5, w8));
     x[14] = cmul(x[14], cmul(w6, w8));
     x[15] = cmul(x[15], cmul(w7, w8));
+#endif
 }
 
 // shared-memory address of element f of row t: rows padded so T-fastest lane
@@ -267,7 +290,13 @@ __device__ __forceinline__ double2 root_pi(uint32_t e, int t) {
 }
 
 // Build the tile's twiddle tables: omega^(al_t + be_t*(j + r*NB)) = A[t][j] * B[t][r]
-// (computed at tile start; the stages' barriers publish them).
+//   MOA_PTW_SINCOS 1: sincospi of the exact rational exponent (FP64 work, no loads);
+//   MOA_PTW_SINCOS 0: the plan's two-level omega_n table (2 loads + 1 product)
+#ifndef MOA_PTW_SINCOS
+#define MOA_PTW_SINCOS 1
+#endif
+// (computed at tile start from the plan's two-level omega_n table -- one product per
+// entry; the stages' barriers publish them).
 template <int F, int T>
 __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 *twa, double2 *twb, uint32_t al,
                                                      uint32_t be) {
@@ -278,11 +307,19 @@ __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 
         if (i < T * NB) {
             const int t = i / NB, j = i % NB;
             const uint32_t a = al + (uint32_t)t * (uint32_t)d.a_t, b = be + (uint32_t)t * (uint32_t)d.b_t;
+#if MOA_PTW_SINCOS
             twa[t * (NB + 1) + j] = root_pi((a + b * (uint32_t)j) & nm, d.tbits);
+#else
+            twa[t * (NB + 1) + j] = tw2(d.tw_hi, d.tw_lo, (a + b * (uint32_t)j) & nm, d.hbits);
+#endif
         } else {
             const int k = i - T * NB, t = k / RS, r = k % RS;
             const uint32_t b = be + (uint32_t)t * (uint32_t)d.b_t;
+#if MOA_PTW_SINCOS
             twb[t * (RS + 1) + r] = root_pi((b * (uint32_t)(NB * r)) & nm, d.tbits);
+#else
+            twb[t * (RS + 1) + r] = tw2(d.tw_hi, d.tw_lo, (b * (uint32_t)(NB * r)) & nm, d.hbits);
+#endif
         }
     }
 }
@@ -330,23 +367,29 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     // ---- gather inputs (the first stage then builds the tile's twiddle tables while
     //      its loads are in flight)
     if constexpr (FIRST && SRC == 0) {
-        const unsigned cm = d.conj_in ? 0x80000000u : 0u;
-        const int64_t sf = (int64_t)NB * d.in_f;
+        // element offsets inside the tile's span fit 32 bits (span < n <= 2^32)
+        const uint32_t sf = (uint32_t)NB * (uint32_t)d.in_f;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            const double2 *p = c.in + (int64_t)tt[i] * d.in_t + (int64_t)jj[i] * d.in_f;
+            const double2 *p = elem_off(c.in, (uint32_t)tt[i] * (uint32_t)d.in_t + (uint32_t)jj[i] * (uint32_t)d.in_f);
 #pragma unroll
-            for (int r = 0; r < RS; ++r) x[i * RS + r] = conj_mask(ld_io<LD>(p + r * sf, pol), cm);
+            for (int r = 0; r < RS; ++r) x[i * RS + r] = ld_io<LD>(elem_off_c(p, r, sf), pol);
+        }
+        if (d.conj_in) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
     } else if constexpr (FIRST) {
-        const unsigned cm = d.conj_in ? 0x80000000u : 0u;
 #pragma unroll
         for (int i = 0; i < M; ++i)
 #pragma unroll
-            for (int r = 0; r < RS; ++r)
-                x[i * RS + r] = conj_mask(inbuf[stage_idx<F, T, SRC>(tt[i], jj[i] + r * NB)], cm);
+            for (int r = 0; r < RS; ++r) x[i * RS + r] = inbuf[stage_idx<F, T, SRC>(tt[i], jj[i] + r * NB)];
+        if (d.conj_in) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
+        }
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         hook();
     } else {
@@ -391,8 +434,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         }
         __syncthreads();
     } else {
-        const unsigned cm = d.conj_out ? 0x80000000u : 0u;
-        const int64_t so = (int64_t)NB * d.out_k;
+        const uint32_t so = (uint32_t)NB * (uint32_t)d.out_k;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const int t = tt[i], j = jj[i];
@@ -403,17 +445,21 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
                 for (int r = 1; r < RS; ++r) v[r] = cmul(v[r], cmul(a, c.twb[t * (RS + 1) + r]));
             }
+            if (d.conj_out) {
+#pragma unroll
+                for (int r = 0; r < RS; ++r) v[r].y = -v[r].y;
+            }
             if (d.pack_lp >= 0) {   // general pack (single-level local transform, p > 1)
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
                     const int64_t K = c.k_base + (int64_t)t * d.K_t + (int64_t)(j + r * NB) * d.K_k;
                     const int64_t addr = (K & ((1ll << d.pack_lp) - 1)) * d.pack_chunk + (K >> d.pack_lp);
-                    st_io<ST>(c.out + addr, conj_mask(v[r], cm), pol);
+                    st_io<ST>(c.out + addr, v[r], pol);
                 }
             } else {
-                double2 *po = c.out + (int64_t)t * d.out_t + (int64_t)j * d.out_k;
+                double2 *po = elem_off(c.out, (uint32_t)t * (uint32_t)d.out_t + (uint32_t)j * (uint32_t)d.out_k);
 #pragma unroll
-                for (int r = 0; r < RS; ++r) st_io<ST>(po + r * so, conj_mask(v[r], cm), pol);
+                for (int r = 0; r < RS; ++r) st_io<ST>(elem_off_c(po, r, so), v[r], pol);
             }
         }
     }
@@ -432,10 +478,10 @@ __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDe
 template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
 __device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDesc &d, const TileIO &io, int64_t b,
                                          const double2 *inbuf = nullptr, const Hook &hook = Hook()) {
-    const int64_t u = b % d.U;
-    b /= d.U;
-    const int64_t v = b % d.V;
-    const int64_t w = b / d.V;
+    // U and V are powers of two: decode with shifts and masks
+    const int64_t u = b & (d.U - 1);
+    const int64_t v = (b >> d.lU) & (d.V - 1);
+    const int64_t w = b >> (d.lU + d.lV);
     TileCtx c;
     c.in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
     c.out = io.dst + (u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
@@ -502,11 +548,9 @@ template <int F, int T, int SRC>
 __device__ __forceinline__ void tma_issue_tile(const CUtensorMap *map, uint64_t *bar, double2 *inbuf,
                                                const PassDesc &d, int64_t tile) {
     using TS = TmaShape<F, T, SRC>;
-    int64_t b = tile;
-    const int u = (int)(b % d.U);
-    b /= d.U;
-    const int v = (int)(b % d.V);
-    const int w = (int)(b / d.V);
+    const int u = (int)(tile & (d.U - 1));
+    const int v = (int)((tile >> d.lU) & (d.V - 1));
+    const int w = (int)(tile >> (d.lU + d.lV));
     mbar_expect_tx(bar, TS::BOX_BYTES * TS::NBOX);
 #pragma unroll
     for (int k = 0; k < TS::NBOX; ++k) {

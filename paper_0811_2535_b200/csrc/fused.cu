@@ -28,6 +28,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
+// release-ordered increment: the CTA's prior writes (ordered before this thread
+// by the preceding __syncthreads) are visible to any thread that acquires the new value
+__device__ __forceinline__ void red_release_add(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ void wait_geq(const unsigned long long *p, unsigned long long target) {
     if (ld_acquire_u64(p) >= target) return;
     unsigned ns = 32;
@@ -164,9 +170,91 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ticket variant: one work item per CTA, no TMA, no persistence.  Each CTA
+// takes the next ticket from a global counter, so every item with a smaller
+// ticket already belongs to a resident CTA: waiting on it cannot deadlock.
+// The tile itself is the plain pass tile (register gathers straight from
+// global memory), which keeps 4 CTAs per SM resident like fft_pass_kernel.
+//   middle-pass item: work (HBM, evict-first) -> scratch slot (L2)
+//   last-pass item:   scratch slot (L2, ld.cg) -> out (HBM, streaming store),
+//                     then the consumed scratch lines are discarded from L2.
+template <int F2, int T2, int F3, int T3>
+struct TicketShape {
+    static constexpr int NT = PassShape<F2, T2>::NT;
+    static_assert(PassShape<F3, T3>::NT == NT, "fused passes need equal block sizes");
+    static constexpr size_t SMEM = PassShape<F2, T2>::SMEM > PassShape<F3, T3>::SMEM ? PassShape<F2, T2>::SMEM
+                                                                                      : PassShape<F3, T3>::SMEM;
+    static constexpr size_t XCH2 = PassShape<F2, T2>::XCH, XCH3 = PassShape<F3, T3>::XCH;
+    static constexpr int MINB = PassShape<F2, T2>::MINB < PassShape<F3, T3>::MINB ? PassShape<F2, T2>::MINB
+                                                                                  : PassShape<F3, T3>::MINB;
+};
+
+template <int F2, int T2, int F3, int T3>
+__global__ void __launch_bounds__(TicketShape<F2, T2, F3, T3>::NT, TicketShape<F2, T2, F3, T3>::MINB)
+    fused_ticket_kernel(const FusedDesc fd) {
+    using SH = TicketShape<F2, T2, F3, T3>;
+    extern __shared__ double2 sm[];
+    __shared__ int s_code;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        // ticket: blockIdx (CTAs are dispatched in index order, so every smaller
+        // index is resident or finished) or, with fd.ticket == 2, a global counter
+        const unsigned long long ticket =
+            fd.ticket == 2 ? atomicAdd(fd.claim, 1ull) - fd.epoch * (unsigned long long)fd.total_items : blockIdx.x;
+        const int code = __ldg(fd.items + ticket);
+        const int kind = code >> 30, g = (code >> 16) & 0x3fff;
+        if (kind == 1) wait_geq(fd.done2 + g, (fd.epoch + 1) * (unsigned long long)fd.tiles2);
+        else if (g >= fd.slots) wait_geq(fd.done3 + (g - fd.slots), (fd.epoch + 1) * (unsigned long long)fd.tiles3);
+        s_code = code;
+    }
+    __syncthreads();
+    const int code = s_code;
+    const int kind = code >> 30, g = (code >> 16) & 0x3fff, tile = code & 0xffff;
+    double2 *slot_ptr = fd.scratch + (int64_t)(g % fd.slots) * fd.rows_per_group_elems;
+    const int64_t shift = (int64_t)g * fd.rows_per_group_elems;
+    if (kind == 0) {
+        TileIO io{fd.work, slot_ptr, 0, shift};
+        tile_fft<F2, T2, 0, NoHook, 2, 0>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH2),
+                                          fd.p2, io, (int64_t)g * fd.tiles2 + tile);
+    } else {
+        TileIO io{slot_ptr, fd.out, shift, 0};
+        tile_fft<F3, T3, 0, NoHook, 1, 1>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH3),
+                                          fd.p3, io, (int64_t)g + (int64_t)fd.groups * tile);
+        if (fd.discard) {
+            __syncthreads();   // every lane has loaded its scratch points
+            constexpr int LINES_PER_SEG = F3 * 16 / 128;
+            for (int i = tid; i < T3 * LINES_PER_SEG; i += SH::NT) {
+                const int t = i / LINES_PER_SEG, l = i % LINES_PER_SEG;
+                const double2 *a = slot_ptr + (int64_t)tile * F3 + (int64_t)t * fd.f2f3 + l * 8;
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) red_release_add((kind == 0 ? fd.done2 : fd.done3) + g, 1ull);
+}
+
+template <int F2, int T2, int F3, int T3>
+static cudaError_t launch_ticket_f(const FusedDesc &fd, cudaStream_t s) {
+    using SH = TicketShape<F2, T2, F3, T3>;
+    static bool attr = false;
+    if (!attr) {
+        if (SH::SMEM > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(fused_ticket_kernel<F2, T2, F3, T3>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    fused_ticket_kernel<F2, T2, F3, T3><<<(unsigned)fd.total_items, SH::NT, SH::SMEM, s>>>(fd);
+    return cudaGetLastError();
+}
+
 template <int F2, int T2, int F3, int T3>
 static cudaError_t launch_f(const FusedDesc &fd, const CUtensorMap &m2, const CUtensorMap &m3, int grid,
                             cudaStream_t s) {
+    if (fd.ticket) return launch_ticket_f<F2, T2, F3, T3>(fd, s);
     using SH = FusedShape<F2, T2, F3, T3>;
     static bool attr = false;
     if (!attr) {

@@ -25,7 +25,8 @@ struct PassDesc {
     const double2 *tw_lo;   // omega_n^e, e < 2^hbits                          (sign -1)
     const double2 *tw_f;    // omega_FMAX^e, e < FMAX: intra-pass stage twiddles (sign -1)
     // tile id -> (u, v, w):  u = id % U, v = (id / U) % V, w = id / (U * V)
-    int64_t U, V;
+    int64_t U, V;           // powers of two
+    int lU, lV;             // log2 U, log2 V
     // input element (tile, t, f): in_u*u + in_v*v + in_w*w + in_t*t + in_f*f
     int64_t in_u, in_v, in_w, in_t, in_f;
     // last pass: output index K = K_u*u + K_v*v + K_w*w + K_t*t + K_k*k
@@ -69,6 +70,7 @@ struct FusedDesc {
     double2 *scratch;            // slots * rows_per_group_elems
     int64_t f2f3;                // elements per row (F2 * F3)
     int discard;                 // L2 discard of consumed scratch lines
+    int ticket;                  // 1: one item per CTA (fused_ticket_kernel); 0: persistent TMA kernel
     const double2 *work;         // middle-pass input (whole view)
     double2 *out;                // last-pass output
 };

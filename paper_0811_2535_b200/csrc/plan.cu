@@ -184,6 +184,10 @@ struct moa_fft_plan_s {
     double2 *tw_hi = nullptr, *tw_lo = nullptr, *tw_f = nullptr;
     double2 *work = nullptr, *send = nullptr, *recv = nullptr;
     double2 *stage_in = nullptr, *stage_out = nullptr;  // execute_host staging
+    // execute_host_batch: second staging pair + copy streams and events (lazily created)
+    double2 *stage_in2 = nullptr, *stage_out2 = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
     int64_t work_elems = 0, send_elems = 0;
     std::vector<PassPlan> passes;   // p == 1: all passes; p > 1: phase 1 for rank `rank`
     std::vector<std::vector<PassPlan>> rank_passes;  // emulated: phase 1 per virtual rank
@@ -417,6 +421,11 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
                 D.out_k = D.K_k / P;
             }
         }
+        if (!pow2(D.U) || !pow2(D.V))
+            return fail(MOA_ERR_INVALID_ARG, "internal: tile grid %lld x %lld not powers of two", (long long)D.U,
+                        (long long)D.V);
+        D.lU = ilog2(D.U);
+        D.lV = ilog2(D.V);
         if (!pass_supported(pp.logF, pp.T))
             return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
         out.push_back(pp);
@@ -438,6 +447,13 @@ static void free_plan(moa_fft_plan_s *pl) {
     cudaFree(pl->recv);
     cudaFree(pl->stage_in);
     cudaFree(pl->stage_out);
+    cudaFree(pl->stage_in2);
+    cudaFree(pl->stage_out2);
+    if (pl->h2d) cudaStreamSynchronize(pl->h2d), cudaStreamDestroy(pl->h2d);
+    if (pl->d2h) cudaStreamSynchronize(pl->d2h), cudaStreamDestroy(pl->d2h);
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t e : {pl->ev_h2d[b], pl->ev_comp[b], pl->ev_d2h[b]})
+            if (e) cudaEventDestroy(e);
     cudaFree(pl->items);
     cudaFree(pl->counters);
     cudaFree(pl->scratch);
@@ -452,7 +468,7 @@ static void free_plan(moa_fft_plan_s *pl) {
 
 // Fuse the last two passes of a 3-level lifting through an L2-resident ring
 // (fused.cu) when a kernel for their (F, T) pair exists; otherwise keep them separate.
-static int setup_fused(moa_fft_plan_s *pl) {
+static int setup_fused(moa_fft_plan_s *pl, int kind) {
     PassPlan &p2 = pl->passes[1], &p3 = pl->passes[2];
     if (!fused_supported(p2.logF, p2.T, p3.logF, p3.T)) return MOA_OK;
     const int64_t F1 = pl->lift[0], F2 = pl->lift[1], F3 = pl->lift[2];
@@ -461,7 +477,8 @@ static int setup_fused(moa_fft_plan_s *pl) {
     const int tiles2 = (int)(F3 / p2.T) * T3;
     const int tiles3 = (int)F2;
     if (groups >= (1 << 14) || tiles2 >= (1 << 16) || tiles3 >= (1 << 16)) return MOA_OK;
-    int slots = env_int("MOA_FFT_SLOTS", 3), lag = env_int("MOA_FFT_LAG", 1);
+    const bool ticket = kind >= 2;   // 2: blockIdx tickets, 3: atomic tickets
+    int slots = env_int("MOA_FFT_SLOTS", ticket ? 4 : 3), lag = env_int("MOA_FFT_LAG", ticket ? 2 : 1);
     if (lag < 0) lag = 0;
     if (slots < lag + 1) slots = lag + 1;
     if (slots > groups) slots = groups;
@@ -500,6 +517,7 @@ static int setup_fused(moa_fft_plan_s *pl) {
     fd.scratch = pl->scratch;
     fd.f2f3 = F2 * F3;
     fd.discard = env_int("MOA_FFT_DISCARD", 1);
+    fd.ticket = ticket ? kind - 1 : 0;
     {   // TMA maps: middle-pass column tiles over `work`, last-pass row tiles over the ring
         PassPlan tmp = p2;
         tmp.tma = 1;
@@ -516,7 +534,7 @@ static int setup_fused(moa_fft_plan_s *pl) {
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(MOA_ERR_CUDA, "scratch tensor map encode failed (%d)", (int)r);
     }
-    pl->fgrid = fused_grid(p2.logF, p2.T, p3.logF, p3.T);
+    pl->fgrid = ticket ? (int)items.size() : fused_grid(p2.logF, p2.T, p3.logF, p3.T);
     int gmax = env_int("MOA_FFT_FGRID", 0);
     if (gmax > 0 && gmax < pl->fgrid) pl->fgrid = gmax;
     if (pl->fgrid <= 0) return fail(MOA_ERR_CUDA, "fused kernel occupancy query failed");
@@ -657,7 +675,8 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
             return rc;
         }
         for (auto &pp : pl->passes) choose_tma(pp);
-        if (p == 1 && pl->d == 3 && env_int("MOA_FFT_FUSE", 0) && (rc = setup_fused(pl)) != MOA_OK) {
+        const int fuse = env_int("MOA_FFT_FUSE", 0);
+        if (p == 1 && pl->d == 3 && fuse && (rc = setup_fused(pl, fuse)) != MOA_OK) {
             free_plan(pl);
             return rc;
         }
@@ -845,6 +864,76 @@ int moa_fft_execute_host(moa_fft_plan_t pl, const void *host_in, void *host_out)
     int rc = moa_fft_execute(pl, pl->stage_in, pl->stage_out);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(host_out, pl->stage_out, bytes, cudaMemcpyDeviceToHost, pl->stream));
+    CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    return MOA_OK;
+}
+
+int moa_fft_execute_host_batch(moa_fft_plan_t pl, int count, const void *const *host_in, void *const *host_out) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    if (count < 0 || (count > 0 && (!host_in || !host_out)))
+        return fail(MOA_ERR_INVALID_ARG, "bad batch (count=%d)", count);
+    for (int i = 0; i < count; ++i)
+        if (!host_in[i] || !host_out[i]) return fail(MOA_ERR_ALIGN, "NULL host buffer at batch index %d", i);
+    if (count == 0) return MOA_OK;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != pl->device) cudaSetDevice(pl->device);
+    struct Restore {
+        int cur, dev;
+        ~Restore() {
+            if (cur != dev) cudaSetDevice(cur);
+        }
+    } restore_{cur, pl->device};
+    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M;
+    size_t bytes = (size_t)elems * sizeof(double2);
+    if (!pl->stage_in) {
+        if (cudaMalloc((void **)&pl->stage_in, bytes) != cudaSuccess ||
+            cudaMalloc((void **)&pl->stage_out, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MOA_ERR_OOM, "staging allocation of 2 x %zu bytes failed", bytes);
+        }
+        pl->workspace_bytes += 2 * (int64_t)bytes;
+    }
+    if (!pl->stage_in2) {
+        if (cudaMalloc((void **)&pl->stage_in2, bytes) != cudaSuccess ||
+            cudaMalloc((void **)&pl->stage_out2, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MOA_ERR_OOM, "second staging allocation of 2 x %zu bytes failed", bytes);
+        }
+        pl->workspace_bytes += 2 * (int64_t)bytes;
+        CUDA_TRY(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_h2d[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_comp[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_d2h[b], cudaEventDisableTiming));
+        }
+    }
+    double2 *din[2] = {pl->stage_in, pl->stage_in2}, *dout[2] = {pl->stage_out, pl->stage_out2};
+    // the copy streams start after everything already queued on the plan stream
+    CUDA_TRY(cudaEventRecord(pl->ev_comp[0], pl->stream));
+    CUDA_TRY(cudaEventRecord(pl->ev_comp[1], pl->stream));
+    CUDA_TRY(cudaEventRecord(pl->ev_d2h[0], pl->stream));
+    CUDA_TRY(cudaEventRecord(pl->ev_d2h[1], pl->stream));
+    // transform i: H2D (copy stream) -> execute (plan stream) -> D2H (copy stream); with
+    // two staging pairs the H2D of i+1 and the D2H of i-1 overlap the execute of i
+    for (int i = 0; i < count; ++i) {
+        const int b = i & 1;
+        CUDA_TRY(cudaStreamWaitEvent(pl->h2d, pl->ev_comp[b], 0));   // din[b] no longer read
+        CUDA_TRY(cudaMemcpyAsync(din[b], host_in[i], bytes, cudaMemcpyHostToDevice, pl->h2d));
+        CUDA_TRY(cudaEventRecord(pl->ev_h2d[b], pl->h2d));
+        CUDA_TRY(cudaStreamWaitEvent(pl->stream, pl->ev_h2d[b], 0));
+        CUDA_TRY(cudaStreamWaitEvent(pl->stream, pl->ev_d2h[b], 0));  // dout[b] drained
+        int rc = execute(pl, din[b], dout[b]);
+        if (rc) return rc;
+        CUDA_TRY(cudaEventRecord(pl->ev_comp[b], pl->stream));
+        CUDA_TRY(cudaStreamWaitEvent(pl->d2h, pl->ev_comp[b], 0));
+        CUDA_TRY(cudaMemcpyAsync(host_out[i], dout[b], bytes, cudaMemcpyDeviceToHost, pl->d2h));
+        CUDA_TRY(cudaEventRecord(pl->ev_d2h[b], pl->d2h));
+    }
+    // the plan stream sees the last D2H complete (so stream-ordered callers are safe), then sync
+    CUDA_TRY(cudaStreamWaitEvent(pl->stream, pl->ev_d2h[(count - 1) & 1], 0));
+    CUDA_TRY(cudaStreamSynchronize(pl->d2h));
     CUDA_TRY(cudaStreamSynchronize(pl->stream));
     return MOA_OK;
 }

@@ -148,7 +148,7 @@ def test_plan_info():
     assert info["passes"] == 3
 
 
-@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
+@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
 def test_variant_kernels_parity(env, monkeypatch):
     """The L2-fused last passes and the TMA-staged passes (env-selected variants)."""
     for k, v in env.items():
@@ -214,6 +214,39 @@ def test_config_2_24_full_parity():
     got = _run(moa.Plan(1 << t), x)
     ref = oracle.fft(x, -1, threads=8)
     assert oracle.rel_l2(got, ref) <= tol(t)
+
+
+@pytest.mark.parametrize("t", [23, 25, 26])
+def test_large_sizes_full_parity(t):
+    """C5 sweep points above the exhaustive range, element by element against Fig 3.9."""
+    x = moa_inputs.signal_for(t)
+    got = _run(moa.Plan(1 << t), x)
+    ref = oracle.fft(x, -1, threads=oracle.max_threads())
+    assert oracle.rel_l2(got, ref) <= tol(t)
+
+
+@pytest.mark.parametrize("t", [27, 28, 29])
+def test_large_sizes_sampled_bins(t):
+    """C5 sweep, 2^27..2^29: sampled bins against the plain definition (long double),
+    Parseval on the whole output, and the device round trip FFT_+1(FFT_-1 x)/n = x."""
+    n = 1 << t
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(moa_inputs.seed_for(t), n, x)
+    plan = moa.Plan(n)
+    out = plan.execute(x)
+    torch.cuda.synchronize()
+    ks = np.array([0, 1, 3, 4097, n // 3, n // 2 + 7, n - 1])
+    got = out[torch.from_numpy(ks).cuda()].cpu().numpy()
+    ref = oracle.dft_bins(x.cpu().numpy(), ks)
+    assert oracle.rel_l2(got, ref) <= tol(t)
+    lhs = torch.sum(out.abs() ** 2).item()
+    rhs = n * torch.sum(x.abs() ** 2).item()
+    assert abs(lhs - rhs) / rhs <= 1e-12
+    inv = moa.Plan(n, 1, +1)
+    back = inv.execute(out)
+    back /= n
+    err = (torch.linalg.vector_norm(back - x) / torch.linalg.vector_norm(x)).item()
+    assert err <= 2 * tol(t)
 
 
 @pytest.mark.slow

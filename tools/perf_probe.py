@@ -35,12 +35,21 @@ def time_plan(t, lift, reps=10, mode=moa.MODE_LIFTED, flush=True):
         ts.append(a.elapsed_time(b) * 1e-3)
     ts.sort()
     tmed = ts[len(ts) // 2]
+    plan.set_profiling(True)
+    plan.get_profile()
+    for _ in range(reps):
+        if flush:
+            fl.fill_(1.0)
+        plan.execute(x, out)
+    kern = [(k["name"], round(k["avg_us"], 1), round(k["alg_bytes"] / k["avg_us"] / 1e3, 1))
+            for k in plan.get_profile()]
+    plan.set_profiling(False)
     info = plan.info()
     gbs = info["hbm_bytes"] / tmed / 1e9
     gf = 5 * n * t / tmed / 1e9
     return {"t": t, "lift": info["lift"], "mode": mode, "us": round(tmed * 1e6, 1),
             "us_min": round(ts[0] * 1e6, 1), "alg_GBps": round(gbs, 1), "GFLOPs": round(gf, 1),
-            "tf": os.environ.get("MOA_FFT_TF", "8192")}
+            "tf": os.environ.get("MOA_FFT_TF", "8192"), "kernels": kern}
 
 
 def calibrate():
