@@ -175,10 +175,12 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def config_block(t: int, world: int, info):
+def config_block(t: int, world: int, info, exchange: str = "nccl"):
     c = {"workload": f"fft1d_c2c_forward_n2^{t}", "n": 1 << t, "p": world,
          "input": "i.i.d. uniform [-1,1) re/im, SplitMix64 seed 0x08112535+t",
-         "parallelism": (f"reshape-transpose p={world} (NCCL all-to-all)" if world > 1 else "single GPU"),
+         "parallelism": ((f"reshape-transpose p={world} (" + ("fused NVLink push + 8 B NCCL barrier"
+                                                              if exchange == "p2p" else "NCCL all-to-all")
+                          + ")") if world > 1 else "single GPU"),
          "l2": "working set (in + out + scratch = 768 MiB at 2^24) larger than the 126 MB L2; no flush"}
     if info is not None:
         c["lift"] = info["lift"]
@@ -207,7 +209,10 @@ def run_ours(args, rank: int, world: int):
     moa.gen_uniform(moa_inputs.seed_for(t), M, x, first=rank, stride=world)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream(device=dev)
-    plan = moa.Plan(n, world, -1, stream=stream)
+    xchg = moa.XCHG_P2P if (world > 1 and args.exchange == "p2p") else moa.XCHG_NCCL
+    plan = moa.Plan(n, world, -1, stream=stream, exchange=xchg)
+    if xchg == moa.XCHG_P2P:
+        plan.enable_p2p()
     info = plan.info()
     lib = moa.load()
 
@@ -298,7 +303,7 @@ def run_ours(args, rank: int, world: int):
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_block(t, world, info),
+                "config": config_block(t, world, info, args.exchange),
                 "hbm": {"alg_bytes_per_step": int(info["hbm_bytes"]),
                         "alg_GBps": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9, 1),
                         "frac_of_measured": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9
@@ -334,6 +339,9 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="p > 1 global transpose: NCCL send/recv group, or the last pass storing into the "
+                         "peers' receive buffers over CUDA-IPC/NVLink (MOA_XCHG_P2P)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules; using 3", file=sys.stderr)

@@ -59,11 +59,27 @@ enum {
                               kernels, the all-to-all done with device copies (tests)    */
 };
 
+/* Global transpose (S7, the Fig 5.9 redistribution) for p > 1. */
+enum {
+    MOA_XCHG_NCCL = 0,     /* last pass packs a send buffer; one NCCL send/recv group   */
+    MOA_XCHG_P2P = 1,      /* last pass stores straight into every peer's receive buffer
+                              through CUDA-IPC-mapped NVLink pointers (the all-to-all is
+                              fused into the butterfly kernel); an 8-byte NCCL all-reduce
+                              is the only collective (a barrier).  EMULATED plans: the
+                              same stores into the virtual ranks' receive buffers.      */
+    MOA_XCHG_P2P_EXTERNAL = 2  /* as P2P, but no NCCL at all: the caller supplies the
+                              rank (options.rank), exchanges the IPC handles
+                              (moa_fft_ipc_handle / moa_fft_ipc_open) and synchronises
+                              all ranks between moa_fft_execute_phase 1 and 2          */
+};
+
 typedef struct {
     int mode;            /* MOA_MODE_*                                                */
     int nlift;           /* 0 = default lifting; else number of factors in lift[]      */
     int64_t lift[4];     /* lifting <F1..Fd> (powers of two, product n (p=1) or n/p)   */
     int chunks;          /* p > 1: all-to-all chunks G (0 = default)                   */
+    int exchange;        /* MOA_XCHG_* (p > 1)                                         */
+    int rank;            /* MOA_XCHG_P2P_EXTERNAL: this process's rank in [0, p)       */
 } moa_fft_options;
 
 typedef struct {
@@ -175,6 +191,41 @@ int moa_fft_get_profile(moa_fft_plan_t plan, moa_fft_kernel_stat *stats, int max
  */
 int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opts, int pass,
                           int64_t *in_idx, int64_t *out_idx, int64_t *tw_exp, int64_t *F_out);
+
+/*
+ * Peer-to-peer exchange setup (MOA_XCHG_P2P / MOA_XCHG_P2P_EXTERNAL plans).
+ *   moa_fft_ipc_handle: write the 64-byte cudaIpcMemHandle of this rank's receive
+ *       buffers (plan-owned, 2 x n/p elements: double-buffered across executes) to
+ *       handle_out.
+ *   moa_fft_ipc_open: handles = p consecutive 64-byte handles in rank order (this
+ *       rank's own entry is ignored); maps every peer's receive buffers into this
+ *       process (cudaIpcOpenMemHandle, peer access enabled lazily).  Unmapped by
+ *       moa_fft_destroy.
+ *   moa_fft_enable_p2p: both steps at once, the handles all-gathered over the
+ *       library's NCCL communicator (collective; MOA_XCHG_P2P plans).
+ * Errors: MOA_ERR_INVALID_ARG (not a P2P plan, NULL buffer), MOA_ERR_CUDA (IPC),
+ * MOA_ERR_NO_DIST / MOA_ERR_NCCL (enable_p2p without or with a failing communicator).
+ */
+int moa_fft_ipc_handle(moa_fft_plan_t plan, void *handle_out_64B);
+int moa_fft_ipc_open(moa_fft_plan_t plan, const void *handles_p_x_64B);
+int moa_fft_enable_p2p(moa_fft_plan_t plan);
+
+/*
+ * Split execute of a P2P plan, for callers that synchronise the ranks
+ * themselves (MOA_XCHG_P2P_EXTERNAL):
+ *   phase 1: S5 local lifted passes of `in`; the last pass scales by
+ *            omega_n^(rank*K) (S6) and stores every element into its destination
+ *            rank's receive buffer (S7, fused).  `out` is ignored.
+ *   phase 2: S8 P-point combine of this rank's receive buffer into `out`.
+ * Between its phase 1 and phase 2 every rank must wait until all ranks' phase 1
+ * work has completed (e.g. cudaStreamSynchronize + a host barrier).  Calls
+ * alternate 1, 2, 1, 2, ...; the receive buffers alternate per pair, so one
+ * barrier per execute suffices.  moa_fft_execute on a MOA_XCHG_P2P plan is
+ * phase 1 + an NCCL barrier + phase 2.  Returns MOA_OK, MOA_ERR_INVALID_ARG
+ * (wrong plan kind, handles not opened, phase not 1 or 2), MOA_ERR_ALIGN,
+ * MOA_ERR_CUDA.
+ */
+int moa_fft_execute_phase(moa_fft_plan_t plan, const void *in, void *out, int phase);
 
 /* Thread-local description of the last error ("" if none). */
 const char *moa_fft_last_error(void);

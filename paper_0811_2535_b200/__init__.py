@@ -18,9 +18,11 @@ import os
 from . import build as _build
 
 __all__ = ["Plan", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
-           "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "lib_path", "load"]
+           "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
+           "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
 MODE_LIFTED, MODE_LITERAL, MODE_EMULATED = 0, 1, 2
+XCHG_NCCL, XCHG_P2P, XCHG_P2P_EXTERNAL = 0, 1, 2
 _ERRS = {-1: "INVALID_N", -2: "INVALID_P", -3: "INVALID_SIGN", -4: "ALIGN", -5: "NO_DIST",
          -6: "OOM", -7: "CUDA", -8: "NCCL", -9: "INVALID_ARG"}
 
@@ -33,7 +35,7 @@ class MoaError(RuntimeError):
 
 class _Options(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("nlift", ctypes.c_int), ("lift", ctypes.c_int64 * 4),
-                ("chunks", ctypes.c_int)]
+                ("chunks", ctypes.c_int), ("exchange", ctypes.c_int), ("rank", ctypes.c_int)]
 
 
 class _KernelStat(ctypes.Structure):
@@ -52,7 +54,8 @@ class _Info(ctypes.Structure):
 EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host", "moa_fft_execute_host_batch",
            "moa_fft_destroy", "moa_fft_set_stream", "moa_fft_plan_info", "moa_fft_last_error",
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
-           "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass"]
+           "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
+           "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase"]
 
 _lib = None
 
@@ -79,6 +82,10 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_execute.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host_batch.argtypes = [vp, ci, vp, vp]
+    lib.moa_fft_ipc_handle.argtypes = [vp, vp]
+    lib.moa_fft_ipc_open.argtypes = [vp, vp]
+    lib.moa_fft_enable_p2p.argtypes = [vp]
+    lib.moa_fft_execute_phase.argtypes = [vp, vp, vp, ci]
     lib.moa_fft_destroy.argtypes = [vp]
     lib.moa_fft_destroy.restype = None
     lib.moa_fft_set_stream.argtypes = [vp, vp]
@@ -118,11 +125,13 @@ class Plan:
     """
 
     def __init__(self, n: int, p: int = 1, sign: int = -1, mode: int = MODE_LIFTED,
-                 lift=None, chunks: int = 0, stream=None):
+                 lift=None, chunks: int = 0, stream=None, exchange: int = XCHG_NCCL, rank: int = 0):
         lib = load()
         opt = _Options()
         opt.mode = mode
         opt.chunks = chunks
+        opt.exchange = exchange
+        opt.rank = rank
         if lift:
             opt.nlift = len(lift)
             for i, f in enumerate(lift):
@@ -132,6 +141,7 @@ class Plan:
             raise MoaError(-9, lib.moa_fft_last_error().decode())
         self._h = h
         self.n, self.p, self.sign, self.mode = int(n), int(p), int(sign), mode
+        self.exchange, self.rank = int(exchange), int(rank)
         self._stream = None
         self.set_stream(stream)
 
@@ -190,6 +200,43 @@ class Plan:
         if rc:
             _err(rc)
         return host_outs
+
+    def ipc_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's receive buffers (P2P plans)."""
+        buf = (ctypes.c_char * 64)()
+        rc = _lib.moa_fft_ipc_handle(self._h, buf)
+        if rc:
+            _err(rc)
+        return bytes(buf)
+
+    def ipc_open(self, handles):
+        """Map every peer's receive buffers (handles: p 64-byte handles in rank order)."""
+        blob = b"".join(handles)
+        rc = _lib.moa_fft_ipc_open(self._h, ctypes.c_char_p(blob))
+        if rc:
+            _err(rc)
+
+    def enable_p2p(self, group=None):
+        """Exchange the IPC handles and map the peers.  With the library's NCCL
+        communicator (MOA_XCHG_P2P) the library does it; otherwise (P2P_EXTERNAL)
+        torch.distributed all-gathers the handles."""
+        if self.exchange == XCHG_P2P:
+            rc = _lib.moa_fft_enable_p2p(self._h)
+            if rc:
+                _err(rc)
+            return
+        import torch.distributed as dist
+        hs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(hs, self.ipc_handle(), group=group)
+        self.ipc_open(hs)
+
+    def execute_phase(self, x, out, phase: int):
+        """Phase 1 (local passes + fused push into the peers) or 2 (P-point combine)."""
+        rc = _lib.moa_fft_execute_phase(self._h, _ptr(x) if x is not None else None,
+                                        _ptr(out) if out is not None else None, int(phase))
+        if rc:
+            _err(rc)
+        return out
 
     def set_profiling(self, enable: bool = True):
         """Bracket every kernel launch with CUDA events (moa_fft_set_profiling)."""

@@ -36,11 +36,14 @@ struct NcclApi {
     ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
 NcclApi g_nccl;
 ncclComm_t g_comm = nullptr;
+double *g_barrier_buf = nullptr;   // 8-byte device word the barrier all-reduces
 int g_rank = -1, g_size = 0;
 
 int load_nccl(std::string *err) {
@@ -69,6 +72,8 @@ int load_nccl(std::string *err) {
     SYM(GroupStart, "ncclGroupStart");
     SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(AllGather, "ncclAllGather");
 #undef SYM
     g_nccl.handle = h;
     return MOA_OK;
@@ -127,6 +132,45 @@ int dist_alltoall(const double2 *send, double2 *recv, int64_t chunk, int p, int 
     return MOA_OK;
 }
 
+// Stream-ordered barrier of all ranks (the P2P exchange's only collective): an
+// 8-byte all-reduce completes on a rank only after every rank has enqueued it,
+// i.e. after every rank's preceding kernels (the fused push) have finished.
+int dist_barrier(cudaStream_t s, std::string *err) {
+    if (!g_comm) {
+        *err = "no communicator (moa_dist_init)";
+        return MOA_ERR_NO_DIST;
+    }
+    if (!g_barrier_buf && cudaMalloc((void **)&g_barrier_buf, sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        *err = "barrier buffer allocation failed";
+        return MOA_ERR_OOM;
+    }
+    ncclResult_t r = g_nccl.AllReduce(g_barrier_buf, g_barrier_buf, 1, kNcclFloat64, 0 /* sum */, g_comm, s);
+    if (r) {
+        *err = nccl_msg("ncclAllReduce (barrier)", r);
+        return MOA_ERR_NCCL;
+    }
+    return MOA_OK;
+}
+
+// all-gather `bytes` per rank between device buffers, synchronous (plan setup only)
+int dist_allgather_sync(const void *send_dev, void *recv_dev, size_t bytes, cudaStream_t s, std::string *err) {
+    if (!g_comm) {
+        *err = "no communicator (moa_dist_init)";
+        return MOA_ERR_NO_DIST;
+    }
+    ncclResult_t r = g_nccl.AllGather(send_dev, recv_dev, bytes, 1 /* ncclUint8 */, g_comm, s);
+    if (r) {
+        *err = nccl_msg("ncclAllGather", r);
+        return MOA_ERR_NCCL;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+        *err = "stream synchronize after ncclAllGather failed";
+        return MOA_ERR_CUDA;
+    }
+    return MOA_OK;
+}
+
 }  // namespace moa
 
 extern "C" {
@@ -164,6 +208,10 @@ int moa_dist_init(int rank, int p, const void *id_128B) {
 }
 
 int moa_dist_finalize(void) {
+    if (g_barrier_buf) {
+        cudaFree(g_barrier_buf);
+        g_barrier_buf = nullptr;
+    }
     if (g_comm) {
         g_nccl.CommDestroy(g_comm);
         g_comm = nullptr;

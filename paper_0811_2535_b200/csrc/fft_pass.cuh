@@ -242,7 +242,8 @@ template <int ST>
 __device__ __forceinline__ void st_io(double2 *p, double2 v, unsigned long long pol) {
     if constexpr (ST == 1) __stcs(p, v);
     else if constexpr (ST == 2) st_hint(p, v, pol);
-    else *p = v;
+    else   // explicit st.global (a peer pointer must not become a generic store)
+        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
 // Input staging layouts of a TMA-loaded tile (SRC != 0):
@@ -453,8 +454,10 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
                     const int64_t K = c.k_base + (int64_t)t * d.K_t + (int64_t)(j + r * NB) * d.K_k;
-                    const int64_t addr = (K & ((1ll << d.pack_lp) - 1)) * d.pack_chunk + (K >> d.pack_lp);
-                    st_io<ST>(c.out + addr, v[r], pol);
+                    const int64_t dst = K & ((1ll << d.pack_lp) - 1);
+                    double2 *a = d.peer[0] ? d.peer[dst] + (d.peer_off + (K >> d.pack_lp))
+                                           : c.out + (dst * d.pack_chunk + (K >> d.pack_lp));
+                    st_io<ST>(a, v[r], pol);
                 }
             } else {
                 double2 *po = elem_off(c.out, (uint32_t)t * (uint32_t)d.out_t + (uint32_t)j * (uint32_t)d.out_k);
@@ -484,7 +487,9 @@ __device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDes
     const int64_t w = b >> (d.lU + d.lV);
     TileCtx c;
     c.in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
-    c.out = io.dst + (u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
+    // fused exchange: tile row v is destination rank v (every row of the tile goes there)
+    c.out = d.peer[0] ? d.peer[v] + (d.peer_off + u * d.out_u + w * d.out_w)
+                      : io.dst + (u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
     c.k_base = u * d.K_u + v * d.K_v + w * d.K_w;
     c.al = (uint32_t)d.a_c + (uint32_t)u * (uint32_t)d.a_u + (uint32_t)v * (uint32_t)d.a_v + (uint32_t)w * (uint32_t)d.a_w;
     c.be = (uint32_t)d.b_c + (uint32_t)u * (uint32_t)d.b_u + (uint32_t)v * (uint32_t)d.b_v + (uint32_t)w * (uint32_t)d.b_w;
@@ -576,8 +581,10 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, (T * F <= 2048) ? MOA_TMA
     fft_pass_tma_kernel(const PassDesc d, const __grid_constant__ CUtensorMap tmap, int64_t tiles) {
     using TS = TmaShape<F, T, SRC>;
     extern __shared__ unsigned char smraw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
-    double2 *buf[2] = {reinterpret_cast<double2 *>(base), reinterpret_cast<double2 *>(base + TS::BUF)};
+    // align by pointer arithmetic (an integer round trip would lose the shared
+    // address space and turn every exchange access into a generic LD/ST)
+    unsigned char *base = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
+    auto buf = [&](int i) { return reinterpret_cast<double2 *>(base + i * TS::BUF); };
     double2 *tw = reinterpret_cast<double2 *>(base + 2 * TS::BUF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(base + 2 * TS::BUF + TS::TW);
     const int tid = threadIdx.x;
@@ -588,18 +595,18 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, (T * F <= 2048) ? MOA_TMA
     }
     __syncthreads();
     int64_t tile = blockIdx.x;
-    if (tid == 0 && tile < tiles) tma_issue_tile<F, T, SRC>(&tmap, &bar[0], buf[0], d, tile);
+    if (tid == 0 && tile < tiles) tma_issue_tile<F, T, SRC>(&tmap, &bar[0], buf(0), d, tile);
     const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
         const int b = it & 1;
-        __syncthreads();   // the previous tile is done with buf[b^1] and the twiddle tables
+        __syncthreads();   // the previous tile is done with buf(b^1) and the twiddle tables
         const int64_t next = tile + gridDim.x;
         if (tid == 0 && next < tiles) {
             fence_proxy_async();
-            tma_issue_tile<F, T, SRC>(&tmap, &bar[b ^ 1], buf[b ^ 1], d, next);
+            tma_issue_tile<F, T, SRC>(&tmap, &bar[b ^ 1], buf(b ^ 1), d, next);
         }
         mbar_wait(&bar[b], (it >> 1) & 1);
-        tile_fft<F, T, SRC, SyncHook>(buf[b], tw, d, io, tile, buf[b], SyncHook());
+        tile_fft<F, T, SRC, SyncHook>(buf(b), tw, d, io, tile, buf(b), SyncHook());
     }
 }
 

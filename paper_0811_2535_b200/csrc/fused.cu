@@ -78,8 +78,10 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
     fused_kernel(const FusedDesc fd, const __grid_constant__ CUtensorMap map2, const __grid_constant__ CUtensorMap map3) {
     using SH = FusedShape<F2, T2, F3, T3>;
     extern __shared__ unsigned char smraw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
-    double2 *buf[2] = {reinterpret_cast<double2 *>(base), reinterpret_cast<double2 *>(base + SH::BUF)};
+    // align by pointer arithmetic (an integer round trip would lose the shared
+    // address space and turn every exchange access into a generic LD/ST)
+    unsigned char *base = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
+    auto buf = [&](int i) { return reinterpret_cast<double2 *>(base + i * SH::BUF); };
     double2 *tw = reinterpret_cast<double2 *>(base + 2 * SH::BUF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(base + 2 * SH::BUF + SH::TW);
     __shared__ long long s_item[2];
@@ -100,10 +102,10 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
             }
             fence_proxy_async_global();   // the generic-proxy scratch writes are visible to TMA
             fence_proxy_async();
-            tma_issue_scratch<F3, T3>(&map3, &bar[b], buf[b], tile, g % fd.slots);
+            tma_issue_scratch<F3, T3>(&map3, &bar[b], buf(b), tile, g % fd.slots);
         } else {
             fence_proxy_async();
-            tma_issue_tile<F2, T2, 1>(&map2, &bar[b], buf[b], fd.p2, (int64_t)g * fd.tiles2 + tile);
+            tma_issue_tile<F2, T2, 1>(&map2, &bar[b], buf(b), fd.p2, (int64_t)g * fd.tiles2 + tile);
         }
         return true;
     };
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
         const int64_t shift = (int64_t)g * fd.rows_per_group_elems;
         if (kind == 0) {
             TileIO io{fd.work, slot_ptr, 0, shift};
-            tile_fft<F2, T2, 1, SyncHook, 0, 0>(buf[b], tw, fd.p2, io, (int64_t)g * fd.tiles2 + tile, buf[b],
+            tile_fft<F2, T2, 1, SyncHook, 0, 0>(buf(b), tw, fd.p2, io, (int64_t)g * fd.tiles2 + tile, buf(b),
                                                SyncHook());
             __syncthreads();
             if (tid == 0) {
@@ -159,8 +161,8 @@ __global__ void __launch_bounds__(FusedShape<F2, T2, F3, T3>::NT, FusedShape<F2,
                 }
             }
             TileIO io{slot_ptr, fd.out, shift, 0};
-            tile_fft<F3, T3, 2, SyncHook, 0, 1>(buf[b], tw, fd.p3, io, (int64_t)g + (int64_t)fd.groups * tile,
-                                               buf[b], SyncHook());
+            tile_fft<F3, T3, 2, SyncHook, 0, 1>(buf(b), tw, fd.p3, io, (int64_t)g + (int64_t)fd.groups * tile,
+                                               buf(b), SyncHook());
             __syncthreads();
             if (tid == 0) {
                 __threadfence();

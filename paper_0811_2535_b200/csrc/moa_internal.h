@@ -51,6 +51,11 @@ struct PassDesc {
     int64_t pack_chunk;
     int64_t in_shift;       // subtracted from every input address (src is a window of the view)
     int64_t out_shift;      // subtracted from every in-place output address (dst is a window)
+    // p > 1 fused exchange (MOA_XCHG_P2P): the element for destination rank dst is
+    // stored at peer[dst] + peer_off + slot (peer[] = the destinations' receive buffers,
+    // NVLink-mapped; peer_off = this rank's source block); NULL peer[0] = send buffer
+    double2 *peer[16];
+    int64_t peer_off;
 };
 
 // L2-fused last two passes (persistent kernel): the middle pass of a 3-level

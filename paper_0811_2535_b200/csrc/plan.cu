@@ -51,6 +51,8 @@ int fail(int code, const char *fmt, ...) {
 int dist_world(int *rank, int *size);
 int dist_alltoall(const double2 *send, double2 *recv, int64_t chunk, int p, int rank, cudaStream_t s,
                   std::string *err);
+int dist_barrier(cudaStream_t s, std::string *err);
+int dist_allgather_sync(const void *send_dev, void *recv_dev, size_t bytes, cudaStream_t s, std::string *err);
 
 // ------------------------------------------------------------------ twiddles
 // exp(-2 pi i e / N) for N a power of two, evaluated in long double on the
@@ -178,6 +180,13 @@ struct moa_fft_plan_s {
     int d = 0;
     int64_t lift[4] = {0, 0, 0, 0};
     int chunks = 1;
+    int exchange = MOA_XCHG_NCCL;
+    // P2P exchange: receive buffers of every rank (own = recv), double-buffered per execute
+    double2 *peer_recv[16] = {};
+    bool peer_mapped[16] = {};   // opened through cudaIpcOpenMemHandle (closed in destroy)
+    bool peers_open = false;
+    int next_phase = 1;
+    unsigned long long xbuf = 0;   // which half of the receive buffers this execute uses
     int device = 0;
     int hbits = 0;
     cudaStream_t stream = nullptr;
@@ -439,6 +448,8 @@ static void free_plan(moa_fft_plan_s *pl) {
     cudaGetDevice(&cur);
     cudaSetDevice(pl->device);
     cudaStreamSynchronize(pl->stream);
+    for (int r = 0; r < 16; ++r)
+        if (pl->peer_mapped[r]) cudaIpcCloseMemHandle(pl->peer_recv[r]);
     cudaFree(pl->tw_hi);
     cudaFree(pl->tw_lo);
     cudaFree(pl->tw_f);
@@ -585,13 +596,21 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     if (mode == MOA_MODE_LITERAL && p != 1)
         return fail(MOA_ERR_INVALID_P, "literal mode is single-GPU (p must be 1, got %d)", p);
     if (mode == MOA_MODE_EMULATED && p < 2) return fail(MOA_ERR_INVALID_P, "emulated mode needs p >= 2");
+    const int exchange = (p > 1 && opt) ? opt->exchange : MOA_XCHG_NCCL;
+    if (exchange < MOA_XCHG_NCCL || exchange > MOA_XCHG_P2P_EXTERNAL)
+        return fail(MOA_ERR_INVALID_ARG, "unknown exchange %d", exchange);
     int rank = 0;
     if (p > 1 && mode != MOA_MODE_EMULATED) {
-        int wr = -1, ws = 0;
-        if (dist_world(&wr, &ws) != MOA_OK || ws == 0)
-            return fail(MOA_ERR_NO_DIST, "p=%d > 1 needs moa_dist_init first", p);
-        if (ws != p) return fail(MOA_ERR_INVALID_P, "p=%d differs from the world size %d", p, ws);
-        rank = wr;
+        if (exchange == MOA_XCHG_P2P_EXTERNAL) {
+            rank = opt->rank;
+            if (rank < 0 || rank >= p) return fail(MOA_ERR_INVALID_ARG, "rank %d outside [0, %d)", rank, p);
+        } else {
+            int wr = -1, ws = 0;
+            if (dist_world(&wr, &ws) != MOA_OK || ws == 0)
+                return fail(MOA_ERR_NO_DIST, "p=%d > 1 needs moa_dist_init first", p);
+            if (ws != p) return fail(MOA_ERR_INVALID_P, "p=%d differs from the world size %d", p, ws);
+            rank = wr;
+        }
     }
     int rc0 = MOA_OK;
     moa_fft_plan_s *pl = new moa_fft_plan_s();
@@ -601,6 +620,7 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     pl->rank = rank;
     pl->sign = sign;
     pl->mode = mode;
+    pl->exchange = exchange;
     pl->M = n / p;
     CUDA_TRY(cudaGetDevice(&pl->device));
     if ((rc0 = resolve_lifting(pl, opt)) != MOA_OK) {
@@ -655,8 +675,11 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
         pl->work_elems = pl->d > 1 ? pl->M : 0;
         if (p > 1) pl->send_elems = (mode == MOA_MODE_EMULATED) ? n : pl->M;
     }
-    if ((rc = alloc(&pl->work, pl->work_elems)) || (rc = alloc(&pl->send, pl->send_elems)) ||
-        (rc = alloc(&pl->recv, pl->send_elems))) {
+    // P2P: no send buffer; real ranks double-buffer the receive buffer (one barrier per execute)
+    const bool p2p = p > 1 && exchange != MOA_XCHG_NCCL;
+    const int64_t recv_elems = p2p && mode != MOA_MODE_EMULATED ? 2 * pl->send_elems : pl->send_elems;
+    if ((rc = alloc(&pl->work, pl->work_elems)) || (rc = alloc(&pl->send, p2p ? 0 : pl->send_elems)) ||
+        (rc = alloc(&pl->recv, recv_elems))) {
         free_plan(pl);
         return rc;
     }
@@ -722,16 +745,23 @@ struct ProfScope {
     }
 };
 
-// launch one pass (plain or TMA-staged) from src to dst
-static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, double2 *dst) {
+// launch one pass (plain or TMA-staged) from src to dst; peers != NULL: the fused
+// exchange stores into peers[dst rank] + peer_off instead of dst
+static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, double2 *dst,
+                     double2 *const *peers = nullptr, int64_t peer_off = 0) {
     PassDesc D = pp.d;
     D.src = src;
     D.dst = dst;
+    if (peers) {
+        for (int r = 0; r < pl->p; ++r) D.peer[r] = peers[r];
+        D.peer_off = peer_off;
+    }
     char name[64];
-    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>", idx, pp.tma ? "_tma" : "", 1 << pp.logF, pp.T);
+    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : "", 1 << pp.logF, pp.T,
+             peers ? "+push" : "");
     ProfScope ps_(pl, name, 32 * pl->M);
     cudaError_t e;
-    if (pp.tma) {
+    if (pp.tma && !peers) {
         if (pp.map_base != (const void *)src) {
             int rc = encode_pass_map(pp, src);
             if (rc) return rc;
@@ -746,13 +776,32 @@ static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *s
     return MOA_OK;
 }
 
-// run the lifted passes of one (virtual) rank: in -> [work] -> out
-static int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in, double2 *out) {
+// run the lifted passes of one (virtual) rank: in -> [work] -> out (or -> peers)
+static int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in, double2 *out,
+                      double2 *const *peers = nullptr, int64_t peer_off = 0) {
     const int d = (int)ps.size();
     for (int i = 0; i < d; ++i) {
-        int rc = launch_pp(pl, ps[i], i, (i == 0) ? in : pl->work, (i == d - 1) ? out : pl->work);
+        const bool last = i == d - 1;
+        int rc = launch_pp(pl, ps[i], i, (i == 0) ? in : pl->work, last ? out : pl->work, last ? peers : nullptr,
+                           peer_off);
         if (rc) return rc;
     }
+    return MOA_OK;
+}
+
+// P2P phase 1 (S5 + S6 + fused S7) / phase 2 (S8) on a real rank
+static int p2p_phase(moa_fft_plan_s *pl, const double2 *in, double2 *out, int phase) {
+    const int P = pl->p;
+    const int64_t M = pl->M, chunk = M / P;
+    const int64_t half = (int64_t)(pl->xbuf & 1) * M;
+    if (phase == 1) {
+        double2 *peers[16];
+        for (int r = 0; r < P; ++r) peers[r] = pl->peer_recv[r] + half;
+        return run_passes(pl, pl->passes, in, nullptr, peers, (int64_t)pl->rank * chunk);
+    }
+    ProfScope sc(pl, "pcombine", 32 * M);
+    CUDA_TRY(launch_pcombine(pl->recv + half, out, chunk, P, pl->sign > 0, pl->stream));
+    pl->xbuf ^= 1;
     return MOA_OK;
 }
 
@@ -792,6 +841,21 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
 
     const int P = pl->p;
     const int64_t M = pl->M, chunk = M / P;
+    if (pl->mode == MOA_MODE_EMULATED && pl->exchange != MOA_XCHG_NCCL) {
+        // fused exchange: virtual rank r's last pass stores straight into every
+        // destination's receive block (recv + d*M + r*chunk)
+        double2 *peers[16];
+        for (int dd = 0; dd < P; ++dd) peers[dd] = pl->recv + dd * M;
+        for (int r = 0; r < P; ++r) {
+            int rc = run_passes(pl, pl->rank_passes[r], in + r * M, nullptr, peers, r * chunk);
+            if (rc) return rc;
+        }
+        for (int dd = 0; dd < P; ++dd) {
+            ProfScope sc(pl, "pcombine", 32 * M);
+            CUDA_TRY(launch_pcombine(pl->recv + dd * M, out + dd * M, chunk, P, pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
     if (pl->mode == MOA_MODE_EMULATED) {
         for (int r = 0; r < P; ++r) {
             int rc = run_passes(pl, pl->rank_passes[r], in + r * M, pl->send + r * M);
@@ -807,6 +871,20 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
             CUDA_TRY(launch_pcombine(pl->recv + dd * M, out + dd * M, chunk, P, pl->sign > 0, s));
         }
         return MOA_OK;
+    }
+    if (pl->exchange != MOA_XCHG_NCCL) {
+        if (pl->exchange == MOA_XCHG_P2P_EXTERNAL)
+            return fail(MOA_ERR_INVALID_ARG, "P2P_EXTERNAL plans run through moa_fft_execute_phase");
+        if (!pl->peers_open) return fail(MOA_ERR_INVALID_ARG, "P2P plan without peers (moa_fft_enable_p2p)");
+        int rc = p2p_phase(pl, in, out, 1);
+        if (rc) return rc;
+        std::string err;
+        {
+            ProfScope sc(pl, "barrier (NCCL 8 B)", 0);
+            rc = dist_barrier(s, &err);
+        }
+        if (rc) return fail(rc, "%s", err.c_str());
+        return p2p_phase(pl, in, out, 2);
     }
     int rc = run_passes(pl, pl->passes, in, pl->send);
     if (rc) return rc;
@@ -939,6 +1017,100 @@ int moa_fft_execute_host_batch(moa_fft_plan_t pl, int count, const void *const *
 }
 
 void moa_fft_destroy(moa_fft_plan_t pl) { free_plan(pl); }
+
+static int p2p_real(moa_fft_plan_t pl) {
+    if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    if (pl->p < 2 || pl->mode != MOA_MODE_LIFTED || pl->exchange == MOA_XCHG_NCCL)
+        return fail(MOA_ERR_INVALID_ARG, "not a P2P-exchange plan (p > 1, lifted, exchange P2P)");
+    return MOA_OK;
+}
+
+int moa_fft_ipc_handle(moa_fft_plan_t pl, void *handle_out) {
+    int rc = p2p_real(pl);
+    if (rc) return rc;
+    if (!handle_out) return fail(MOA_ERR_INVALID_ARG, "NULL handle buffer");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, pl->recv));
+    memcpy(handle_out, &h, sizeof h);
+    return MOA_OK;
+}
+
+int moa_fft_ipc_open(moa_fft_plan_t pl, const void *handles) {
+    int rc = p2p_real(pl);
+    if (rc) return rc;
+    if (!handles) return fail(MOA_ERR_INVALID_ARG, "NULL handles");
+    if (pl->peers_open) return fail(MOA_ERR_INVALID_ARG, "peers already mapped");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->device);
+    for (int r = 0; r < pl->p; ++r) {
+        if (r == pl->rank) {
+            pl->peer_recv[r] = pl->recv;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char *)handles + 64 * r, sizeof h);
+        void *ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaSetDevice(cur);
+            return fail(MOA_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d) failed: %s", r, cudaGetErrorString(e));
+        }
+        pl->peer_recv[r] = (double2 *)ptr;
+        pl->peer_mapped[r] = true;
+    }
+    cudaSetDevice(cur);
+    pl->peers_open = true;
+    return MOA_OK;
+}
+
+int moa_fft_enable_p2p(moa_fft_plan_t pl) {
+    int rc = p2p_real(pl);
+    if (rc) return rc;
+    if (pl->exchange != MOA_XCHG_P2P) return fail(MOA_ERR_INVALID_ARG, "enable_p2p needs a MOA_XCHG_P2P plan");
+    char mine[64];
+    if ((rc = moa_fft_ipc_handle(pl, mine)) != MOA_OK) return rc;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->device);
+    char *dev = nullptr;
+    std::vector<char> all(64 * (size_t)pl->p);
+    std::string err;
+    if (cudaMalloc((void **)&dev, 64 * (size_t)(pl->p + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaSetDevice(cur);
+        return fail(MOA_ERR_OOM, "handle exchange buffer allocation failed");
+    }
+    rc = MOA_OK;
+    if (cudaMemcpy(dev, mine, 64, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = fail(MOA_ERR_CUDA, "handle upload failed");
+    else if ((rc = dist_allgather_sync(dev, dev + 64, 64, pl->stream, &err)) != MOA_OK)
+        fail(rc, "%s", err.c_str());
+    else if (cudaMemcpy(all.data(), dev + 64, all.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = fail(MOA_ERR_CUDA, "handle download failed");
+    cudaFree(dev);
+    cudaSetDevice(cur);
+    if (rc) return rc;
+    return moa_fft_ipc_open(pl, all.data());
+}
+
+int moa_fft_execute_phase(moa_fft_plan_t pl, const void *in, void *out, int phase) {
+    int rc = p2p_real(pl);
+    if (rc) return rc;
+    if (!pl->peers_open) return fail(MOA_ERR_INVALID_ARG, "peers not mapped (moa_fft_ipc_open)");
+    if (phase != 1 && phase != 2) return fail(MOA_ERR_INVALID_ARG, "phase %d must be 1 or 2", phase);
+    if (phase != pl->next_phase) return fail(MOA_ERR_INVALID_ARG, "phase %d out of order (expected %d)", phase,
+                                             pl->next_phase);
+    if (phase == 1 && !aligned16(in)) return fail(MOA_ERR_ALIGN, "in must be a 16-byte aligned device pointer");
+    if (phase == 2 && !aligned16(out)) return fail(MOA_ERR_ALIGN, "out must be a 16-byte aligned device pointer");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != pl->device) cudaSetDevice(pl->device);
+    rc = p2p_phase(pl, (const double2 *)in, (double2 *)out, phase);
+    if (cur != pl->device) cudaSetDevice(cur);
+    if (rc == MOA_OK) pl->next_phase = 3 - phase;
+    return rc;
+}
 
 int moa_fft_set_stream(moa_fft_plan_t pl, void *stream) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");

@@ -197,6 +197,22 @@ def test_emulated_distributed(t, P):
         assert float(np.sqrt(num / den)) <= tol(t), (t, P, sign)
 
 
+@pytest.mark.parametrize("t,P", [(4, 2), (6, 8), (10, 4), (14, 8), (20, 2), (20, 8), (24, 8)])
+def test_emulated_fused_exchange(t, P):
+    """MOA_XCHG_P2P on virtual ranks: the last pass stores straight into the destination
+    ranks' receive blocks (no send buffer, no copies) -- bitwise equal to the packed
+    send-buffer + all-to-all path, and X[r + P i] on rank r."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    ref = oracle.fft(x, -1, threads=8)
+    push = _run(moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=moa.XCHG_P2P), xin)
+    pack = _run(moa.Plan(n, P, -1, mode=moa.MODE_EMULATED), xin)
+    assert np.array_equal(push, pack)
+    got = push.reshape(P, n // P)
+    assert max(oracle.rel_l2(got[r], ref[r::P]) for r in range(P)) <= tol(t)
+
+
 def test_emulated_with_lifting_depth3():
     t, P = 21, 4
     x = moa_inputs.signal_for(t)
