@@ -85,6 +85,42 @@ int MOA_CAT(grid_pass_tma_f, MOA_INST_LOGF)(int T, int src) {
     return 0;
 }
 
+// prefetching persistent variant: F >= 32 (at least two stages)
+cudaError_t MOA_CAT(launch_pass_pf_f, MOA_INST_LOGF)(int T, const PassDesc &d, int64_t tiles, int grid,
+                                                    cudaStream_t s) {
+#define MOA_PF_CASE(TT)                                                              \
+    if (T == TT) {                                                                   \
+        if constexpr (kF >= 32 && TT * kF <= TF_MAX) return launch_one_pf<kF, TT>(d, tiles, grid, s); \
+        return cudaErrorInvalidValue;                                                \
+    }
+    MOA_PF_CASE(1)
+    MOA_PF_CASE(2)
+    MOA_PF_CASE(4)
+    MOA_PF_CASE(8)
+    MOA_PF_CASE(16)
+    MOA_PF_CASE(32)
+    MOA_PF_CASE(64)
+#undef MOA_PF_CASE
+    return cudaErrorInvalidValue;
+}
+
+int MOA_CAT(grid_pass_pf_f, MOA_INST_LOGF)(int T) {
+#define MOA_PF_GRID(TT)                                                         \
+    if (T == TT) {                                                              \
+        if constexpr (kF >= 32 && TT * kF <= TF_MAX) return grid_one_pf<kF, TT>(); \
+        return 0;                                                               \
+    }
+    MOA_PF_GRID(1)
+    MOA_PF_GRID(2)
+    MOA_PF_GRID(4)
+    MOA_PF_GRID(8)
+    MOA_PF_GRID(16)
+    MOA_PF_GRID(32)
+    MOA_PF_GRID(64)
+#undef MOA_PF_GRID
+    return 0;
+}
+
 cudaError_t MOA_CAT(prepare_pass_f, MOA_INST_LOGF)() {
     cudaError_t e;
     if ((e = prepare_t<1>()) != cudaSuccess) return e;

@@ -382,6 +382,18 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         }
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
+    } else if constexpr (FIRST && SRC == 3) {
+        // prefetched by this same thread (cp.async, fft_pass_pf_kernel) into the
+        // exchange layout: its own copies are visible after cp.async.wait_all
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[smem_idx<F, T>(tt[i], jj[i] + r * NB)];
+        if (d.conj_in) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
+        }
+        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
     } else if constexpr (FIRST) {
 #pragma unroll
         for (int i = 0; i < M; ++i)
@@ -406,6 +418,9 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
                 for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[smem_idx<F, T>(tt[i], j + r * NB)];
             }
         }
+        // the exchange buffer is free once every lane has read it: the prefetching
+        // kernel starts the next tile's copy into it here (hook = barrier + cp.async)
+        if constexpr (LAST && SRC == 3) hook();
     }
     // ---- twiddle + radix-RS butterflies in registers
 #pragma unroll
@@ -414,7 +429,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         dft_reg<RS>(x + i * RS);
     }
     if constexpr (!LAST) {
-        if (!FIRST) __syncthreads();   // every lane has read before anyone overwrites
+        if (!FIRST || SRC == 3) __syncthreads();   // every lane has read before anyone overwrites
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const int j = jj[i];
@@ -509,6 +524,95 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     tile_fft<F, T>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
                    blockIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent pass with the next tile prefetched into the exchange buffer.
+// The exchange buffer is idle from the moment the last stage has read it until
+// the next tile's first stage: each thread starts cp.async copies of its share of
+// the next tile there (global -> shared, no registers held), so the HBM latency
+// of tile i+1 overlaps the last butterflies, the twiddles and the stores of tile
+// i.  Same shared memory and registers as fft_pass_kernel (4 CTAs per SM at
+// F*T = 2048), one CTA per resident slot.
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// this thread's share of `tile`, in the first stage's lane mapping and the exchange layout
+template <int F, int T>
+__device__ __forceinline__ void prefetch_tile(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b) {
+    using SH = PassShape<F, T>;
+    constexpr int RS = F >= 16 ? 16 : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
+    const int64_t u = b & (d.U - 1);
+    const int64_t v = (b >> d.lU) & (d.V - 1);
+    const int64_t w = b >> (d.lU + d.lV);
+    const double2 *in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
+    const uint32_t sf = (uint32_t)NB * (uint32_t)d.in_f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const int bb = threadIdx.x + NT * i;
+        const bool tfast = T > 1 && d.in_tfast;
+        const int t = tfast ? bb % T : bb / NB, j = tfast ? bb / T : bb % NB;
+        const double2 *p = elem_off(in, (uint32_t)t * (uint32_t)d.in_t + (uint32_t)j * (uint32_t)d.in_f);
+#pragma unroll
+        for (int r = 0; r < RS; ++r) cp_async16(sm + smem_idx<F, T>(t, j + r * NB), elem_off_c(p, r, sf));
+    }
+}
+
+template <int F, int T>
+struct PrefetchHook {
+    double2 *sm;
+    const PassDesc *d;
+    const TileIO *io;
+    int64_t next, tiles;
+    __device__ __forceinline__ void operator()() const {
+        __syncthreads();   // every lane has read the exchange buffer
+        if (next < tiles) prefetch_tile<F, T>(sm, *d, *io, next);
+        cp_async_commit();
+    }
+};
+
+template <int F, int T>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_pf_kernel(const PassDesc d, int64_t tiles) {
+    extern __shared__ double2 sm[];
+    double2 *tw = reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    int64_t tile = blockIdx.x;
+    if (tile >= tiles) return;
+    prefetch_tile<F, T>(sm, d, io, tile);
+    cp_async_commit();
+    for (; tile < tiles; tile += gridDim.x) {
+        cp_async_wait_all();
+        __syncthreads();   // the previous tile's epilogue is done with the twiddle tables
+        const PrefetchHook<F, T> hk{sm, &d, &io, tile + (int64_t)gridDim.x, tiles};
+        tile_fft<F, T, 3, PrefetchHook<F, T>>(sm, tw, d, io, tile, nullptr, hk);
+    }
+}
+
+template <int F, int T>
+cudaError_t launch_one_pf(const PassDesc &d, int64_t tiles, int grid, cudaStream_t s) {
+    using SH = PassShape<F, T>;
+    fft_pass_pf_kernel<F, T><<<grid, SH::NT, SH::SMEM, s>>>(d, tiles);
+    return cudaGetLastError();
+}
+
+template <int F, int T>
+int grid_one_pf() {
+    using SH = PassShape<F, T>;
+    if (SH::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(fft_pass_pf_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM) !=
+            cudaSuccess)
+        return 0;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft_pass_pf_kernel<F, T>, SH::NT, SH::SMEM) !=
+        cudaSuccess)
+        return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
 }
 
 template <int F, int T>

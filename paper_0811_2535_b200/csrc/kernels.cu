@@ -77,6 +77,36 @@ cudaError_t launch_pass_tma(int logF, int T, int src, const PassDesc &d, const C
     }
 }
 
+int pass_pf_grid(int logF, int T) {
+    switch (logF) {
+    case 5: return grid_pass_pf_f5(T);
+    case 6: return grid_pass_pf_f6(T);
+    case 7: return grid_pass_pf_f7(T);
+    case 8: return grid_pass_pf_f8(T);
+    case 9: return grid_pass_pf_f9(T);
+    case 10: return grid_pass_pf_f10(T);
+    case 11: return grid_pass_pf_f11(T);
+    case 12: return grid_pass_pf_f12(T);
+    case 13: return grid_pass_pf_f13(T);
+    default: return 0;
+    }
+}
+
+cudaError_t launch_pass_pf(int logF, int T, const PassDesc &d, int64_t tiles, int grid, cudaStream_t s) {
+    switch (logF) {
+    case 5: return launch_pass_pf_f5(T, d, tiles, grid, s);
+    case 6: return launch_pass_pf_f6(T, d, tiles, grid, s);
+    case 7: return launch_pass_pf_f7(T, d, tiles, grid, s);
+    case 8: return launch_pass_pf_f8(T, d, tiles, grid, s);
+    case 9: return launch_pass_pf_f9(T, d, tiles, grid, s);
+    case 10: return launch_pass_pf_f10(T, d, tiles, grid, s);
+    case 11: return launch_pass_pf_f11(T, d, tiles, grid, s);
+    case 12: return launch_pass_pf_f12(T, d, tiles, grid, s);
+    case 13: return launch_pass_pf_f13(T, d, tiles, grid, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t prepare_pass_kernels() {
     cudaError_t (*fns[])() = {prepare_pass_f1, prepare_pass_f2, prepare_pass_f3, prepare_pass_f4,
                               prepare_pass_f5, prepare_pass_f6, prepare_pass_f7, prepare_pass_f8,

@@ -90,6 +90,9 @@ cudaError_t prepare_pass_kernels();    // raise the dynamic smem limits once
 int pass_tma_grid(int logF, int T, int src);
 cudaError_t launch_pass_tma(int logF, int T, int src, const PassDesc &d, const CUtensorMap &map, int64_t tiles,
                             int grid, cudaStream_t s);
+// prefetching persistent pass (fft_pass_pf_kernel); grid 0 = unsupported
+int pass_pf_grid(int logF, int T);
+cudaError_t launch_pass_pf(int logF, int T, const PassDesc &d, int64_t tiles, int grid, cudaStream_t s);
 int fused_supported(int logF2, int T2, int logF3, int T3);
 cudaError_t launch_fused(int logF2, int T2, int logF3, int T3, const FusedDesc &fd, const CUtensorMap &m2,
                          const CUtensorMap &m3, int grid, cudaStream_t s);
@@ -114,6 +117,8 @@ cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int
     cudaError_t launch_pass_tma_f##f(int T, int src, const PassDesc &d, const CUtensorMap &map, \
                                      int64_t tiles, int grid, cudaStream_t s);              \
     int grid_pass_tma_f##f(int T, int src);                                                 \
+    cudaError_t launch_pass_pf_f##f(int T, const PassDesc &d, int64_t tiles, int grid, cudaStream_t s); \
+    int grid_pass_pf_f##f(int T);                                                           \
     }
 MOA_DECLARE_INST(1)
 MOA_DECLARE_INST(2)

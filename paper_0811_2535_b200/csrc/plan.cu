@@ -89,6 +89,7 @@ struct PassPlan {
     // TMA-staged persistent variant (0 = plain kernel, 1 = column tile, 2 = row tile)
     int tma = 0;
     int tma_grid = 0;
+    int pf_grid = 0;   // > 0: prefetching persistent kernel (fft_pass_pf_kernel)
     CUtensorMap map;
     const void *map_base = nullptr;
 };
@@ -154,9 +155,16 @@ static int encode_pass_map(PassPlan &pp, const void *base) {
     return MOA_OK;
 }
 
-// choose the TMA-staged variant when it exists for this (F, T, layout)
+// choose the TMA-staged variant when it exists for this (F, T, layout), else the
+// prefetching persistent kernel when selected
 static void choose_tma(PassPlan &pp) {
     pp.tma = 0;
+    pp.pf_grid = 0;
+    const char *pf_env = getenv("MOA_FFT_PF");
+    if (pf_env && atoi(pf_env) && pp.logF >= 5) {
+        int g = pass_pf_grid(pp.logF, pp.T);
+        if (g > 0) pp.pf_grid = (int)(g < pp.tiles ? g : pp.tiles);
+    }
     const char *tma_env = getenv("MOA_FFT_TMA");   // measured: the plain kernel (4 CTAs/SM) wins today
     if (!tma_env || atoi(tma_env) == 0) return;
     const PassDesc &D = pp.d;
@@ -241,25 +249,34 @@ static int env_int(const char *name, int dflt) {
     return (s && *s) ? atoi(s) : dflt;
 }
 
-// default lifting <F1..Fd> of a local length 2^tl (SURVEY §8 notation table)
-static int default_lifting(int tl, int64_t *lift) {
+// default lifting <F1..Fd> of a local length 2^tl, from the B200 lifting sweeps
+// (tools/perf_probe.py): 256-point row passes (4 tiles per SM) wherever
+// the length allows, a single first factor up to 2^11, four levels from 2^28 on
+// (two <= 128-point column passes instead of one long one).  p > 1 plans keep <= 3 levels.
+static int default_lifting(int tl, int64_t *lift, int p) {
     if (tl <= FMAX_LOG) {
         lift[0] = (int64_t)1 << tl;
         return 1;
     }
-    if (tl >= 20 && tl <= 16 + FMAX_LOG) {
-        // <2^(tl-16), 256, 256>: 256-point passes keep 4 tiles per SM in flight
-        // (measured fastest at 2^24); MOA_FFT_FUSE=1 runs the last two L2-fused
+    if (tl <= 20) {   // two levels, the longer one last: <256,256> at 2^16, <1024,1024> at 2^20
+        int a = tl / 2;
+        lift[0] = (int64_t)1 << a;
+        lift[1] = (int64_t)1 << (tl - a);
+        return 2;
+    }
+    if (tl <= 27 || (p > 1 && tl <= 16 + FMAX_LOG)) {   // <2^(tl-16), 256, 256>
         lift[0] = (int64_t)1 << (tl - 16);
         lift[1] = 256;
         lift[2] = 256;
         return 3;
     }
-    if (tl <= 2 * (FMAX_LOG - 1) + 2) {   // two levels up to 2^26
-        int a = tl / 2;
+    if (tl <= 16 + 2 * 8 && p == 1) {   // <a, b, 256, 256>, a <= b <= 256
+        int a = (tl - 16) / 2;
         lift[0] = (int64_t)1 << a;
-        lift[1] = (int64_t)1 << (tl - a);
-        return 2;
+        lift[1] = (int64_t)1 << (tl - 16 - a);
+        lift[2] = 256;
+        lift[3] = 256;
+        return 4;
     }
     if (tl <= 3 * FMAX_LOG) {
         int a = tl / 3, b = (tl - a) / 2;
@@ -279,7 +296,9 @@ static int default_lifting(int tl, int64_t *lift) {
 static int choose_T(int logF, int64_t avail) {
     // tile size cap: long transforms take T*F = 8192 (one 128 KiB tile per SM);
     // short ones 4096 (2-3 tiles per SM overlap memory and FP64 work)
-    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : 2048);
+    // measured on B200 (tools/perf_probe.py): 2048-element tiles (4 CTAs/SM) for F <= 256,
+    // 4096 for F = 512, 1024 (T = 8, 4: >= 64-byte column runs), one 8192 tile above
+    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : (logF >= 9 ? 4096 : 2048));
     if (tf_max > TF_MAX) tf_max = TF_MAX;
     int T = 1;
     while (T < 64 && ((int64_t)(2 * T) << logF) <= tf_max && 2 * T <= avail) T *= 2;
@@ -573,7 +592,7 @@ static int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt) {
                         (long long)pl->M);
         pl->d = opt->nlift;
     } else {
-        pl->d = default_lifting(tl, pl->lift);
+        pl->d = default_lifting(tl, pl->lift, p);
     }
     if (p > 1 && pl->lift[0] < p && pl->d > 1)
         return fail(MOA_ERR_INVALID_ARG, "first lifting factor %lld < p=%d", (long long)pl->lift[0], p);
@@ -757,7 +776,8 @@ static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *s
         D.peer_off = peer_off;
     }
     char name[64];
-    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : "", 1 << pp.logF, pp.T,
+    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : ""),
+             1 << pp.logF, pp.T,
              peers ? "+push" : "");
     ProfScope ps_(pl, name, 32 * pl->M);
     cudaError_t e;
@@ -767,6 +787,8 @@ static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *s
             if (rc) return rc;
         }
         e = launch_pass_tma(pp.logF, pp.T, pp.tma, D, pp.map, pp.tiles, pp.tma_grid, pl->stream);
+    } else if (pp.pf_grid > 0) {
+        e = launch_pass_pf(pp.logF, pp.T, D, pp.tiles, pp.pf_grid, pl->stream);
     } else {
         e = launch_pass(pp.logF, pp.T, D, pp.tiles, pl->stream);
     }

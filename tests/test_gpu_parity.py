@@ -144,11 +144,13 @@ def test_plan_info():
     info = moa.Plan(1 << 24, lift=[4096, 4096]).info()
     assert info["passes"] == 2 and info["hbm_bytes"] == 32 * (1 << 24) * 2
     assert info["breakpoint"] == 25
-    info = moa.Plan(1 << 30 if False else 1 << 27).info()
-    assert info["passes"] == 3
+    info = moa.Plan(1 << 27).info()
+    assert info["passes"] == 3 and info["lift"] == [2048, 256, 256]
+    info = moa.Plan(1 << 28).info()   # four levels from 2^28 (DESIGN.md §4 lifting table)
+    assert info["passes"] == 4 and info["lift"] == [64, 64, 256, 256]
 
 
-@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
+@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_PF": "1"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
 def test_variant_kernels_parity(env, monkeypatch):
     """The L2-fused last passes and the TMA-staged passes (env-selected variants)."""
     for k, v in env.items():
