@@ -18,6 +18,8 @@
 // All arithmetic is for sign -1; sign +1 is conj(FFT(conj x)) (conj_in /
 // conj_out flags), so every table is the omega^-e table.
 #pragma once
+#include <stdlib.h>
+
 #include "moa_internal.h"
 #include "tma.cuh"
 
@@ -592,10 +594,34 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     }
 }
 
+// persistent plain pass: the tile loop of fft_pass_kernel without CTA turnover
+template <int F, int T>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_persist_kernel(const PassDesc d, int64_t tiles) {
+    extern __shared__ double2 sm[];
+    double2 *tw = reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        __syncthreads();   // the previous tile is done with the exchange buffer and the tables
+        tile_fft<F, T>(sm, tw, d, io, tile);
+    }
+}
+
 template <int F, int T>
 cudaError_t launch_one_pf(const PassDesc &d, int64_t tiles, int grid, cudaStream_t s) {
     using SH = PassShape<F, T>;
-    fft_pass_pf_kernel<F, T><<<grid, SH::NT, SH::SMEM, s>>>(d, tiles);
+    static const int persist = [] {
+        const char *e = getenv("MOA_FFT_PF");
+        return e && atoi(e) == 2;
+    }();
+    if (persist) {
+        if (SH::SMEM > 48 * 1024)
+            cudaFuncSetAttribute(fft_pass_persist_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SH::SMEM);
+        fft_pass_persist_kernel<F, T><<<grid, SH::NT, SH::SMEM, s>>>(d, tiles);
+    } else {
+        fft_pass_pf_kernel<F, T><<<grid, SH::NT, SH::SMEM, s>>>(d, tiles);
+    }
     return cudaGetLastError();
 }
 

@@ -264,6 +264,12 @@ static int default_lifting(int tl, int64_t *lift, int p) {
         lift[1] = (int64_t)1 << (tl - a);
         return 2;
     }
+    if (tl == 25 || tl == 26) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
+        lift[0] = 256;
+        lift[1] = 256;
+        lift[2] = (int64_t)1 << (tl - 16);
+        return 3;
+    }
     if (tl <= 27 || (p > 1 && tl <= 16 + FMAX_LOG)) {   // <2^(tl-16), 256, 256>
         lift[0] = (int64_t)1 << (tl - 16);
         lift[1] = 256;
