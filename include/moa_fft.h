@@ -80,6 +80,10 @@ typedef struct {
     int chunks;          /* p > 1: all-to-all chunks G (0 = default)                   */
     int exchange;        /* MOA_XCHG_* (p > 1)                                         */
     int rank;            /* MOA_XCHG_P2P_EXTERNAL: this process's rank in [0, p)       */
+    int64_t batch;       /* p == 1, lifted mode: number of independent length-n
+                            transforms stored back to back (transform b at elements
+                            [b*n, (b+1)*n) of in and out); 0 or 1 = one transform.
+                            Every pass covers the whole batch in one launch.           */
 } moa_fft_options;
 
 typedef struct {
@@ -98,6 +102,7 @@ typedef struct {
     int64_t workspace_bytes;  /* device bytes the plan owns                            */
     int64_t hbm_bytes;        /* algorithmic HBM bytes per execute on this rank        */
     int64_t a2a_bytes;        /* bytes this rank sends per execute (p > 1)             */
+    int64_t batch;            /* transforms per execute                                */
 } moa_fft_info;
 
 /*
@@ -118,8 +123,8 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
 
 /*
  * Execute the transform, asynchronously on the plan's stream.
- *   p == 1: in/out hold n elements in natural order; in == out allowed; in is
- *           not modified when in != out.
+ *   p == 1: in/out hold batch*n elements (batch transforms back to back, natural
+ *           order); in == out allowed; in is not modified when in != out.
  *   p > 1 : in/out hold n/p elements of THIS rank in the cyclic layout
  *           in[j] = x[rank + p*j], out[i] = X[rank + p*i] (the paper's xcyclic,
  *           P:799).  Collective: every rank calls it in the same order.

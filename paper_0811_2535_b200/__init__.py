@@ -35,7 +35,8 @@ class MoaError(RuntimeError):
 
 class _Options(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("nlift", ctypes.c_int), ("lift", ctypes.c_int64 * 4),
-                ("chunks", ctypes.c_int), ("exchange", ctypes.c_int), ("rank", ctypes.c_int)]
+                ("chunks", ctypes.c_int), ("exchange", ctypes.c_int), ("rank", ctypes.c_int),
+                ("batch", ctypes.c_int64)]
 
 
 class _KernelStat(ctypes.Structure):
@@ -48,7 +49,7 @@ class _Info(ctypes.Structure):
                 ("sign", ctypes.c_int), ("mode", ctypes.c_int), ("local_n", ctypes.c_int64),
                 ("passes", ctypes.c_int), ("lift", ctypes.c_int64 * 4), ("breakpoint", ctypes.c_int),
                 ("chunks", ctypes.c_int), ("launches", ctypes.c_int), ("workspace_bytes", ctypes.c_int64),
-                ("hbm_bytes", ctypes.c_int64), ("a2a_bytes", ctypes.c_int64)]
+                ("hbm_bytes", ctypes.c_int64), ("a2a_bytes", ctypes.c_int64), ("batch", ctypes.c_int64)]
 
 
 EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execute_host", "moa_fft_execute_host_batch",
@@ -125,13 +126,15 @@ class Plan:
     """
 
     def __init__(self, n: int, p: int = 1, sign: int = -1, mode: int = MODE_LIFTED,
-                 lift=None, chunks: int = 0, stream=None, exchange: int = XCHG_NCCL, rank: int = 0):
+                 lift=None, chunks: int = 0, stream=None, exchange: int = XCHG_NCCL, rank: int = 0,
+                 batch: int = 1):
         lib = load()
         opt = _Options()
         opt.mode = mode
         opt.chunks = chunks
         opt.exchange = exchange
         opt.rank = rank
+        opt.batch = batch
         if lift:
             opt.nlift = len(lift)
             for i, f in enumerate(lift):
@@ -141,7 +144,7 @@ class Plan:
             raise MoaError(-9, lib.moa_fft_last_error().decode())
         self._h = h
         self.n, self.p, self.sign, self.mode = int(n), int(p), int(sign), mode
-        self.exchange, self.rank = int(exchange), int(rank)
+        self.exchange, self.rank, self.batch = int(exchange), int(rank), int(batch)
         self._stream = None
         self.set_stream(stream)
 

@@ -202,7 +202,9 @@ struct PassShape {
 #ifndef MOA_MINB_2048
 #define MOA_MINB_2048 4
 #endif
-    static constexpr int MINB = (T * F <= 2048) ? MOA_MINB_2048 : ((T * F <= 4096) ? 2 : 1);
+    // small tiles: 512 resident threads per SM (<= 128 registers each) whatever the CTA size
+    static constexpr int MINB = (T * F <= 2048) ? (NT >= 128 ? MOA_MINB_2048 : (512 / NT > 16 ? 16 : 512 / NT))
+                                                : ((T * F <= 4096) ? 2 : 1);
 };
 
 // Where one tile reads and writes (a persistent kernel retargets these per tile).
@@ -498,15 +500,21 @@ __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDe
 template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
 __device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDesc &d, const TileIO &io, int64_t b,
                                          const double2 *inbuf = nullptr, const Hook &hook = Hook()) {
+    // batch index above the per-transform tile bits
+    int64_t boff = 0;
+    if (d.bstride) {
+        boff = (b >> d.ltiles) * d.bstride;
+        b &= ((int64_t)1 << d.ltiles) - 1;
+    }
     // U and V are powers of two: decode with shifts and masks
     const int64_t u = b & (d.U - 1);
     const int64_t v = (b >> d.lU) & (d.V - 1);
     const int64_t w = b >> (d.lU + d.lV);
     TileCtx c;
-    c.in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
+    c.in = io.src + (boff + u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
     // fused exchange: tile row v is destination rank v (every row of the tile goes there)
     c.out = d.peer[0] ? d.peer[v] + (d.peer_off + u * d.out_u + w * d.out_w)
-                      : io.dst + (u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
+                      : io.dst + (boff + u * d.out_u + v * d.out_v + w * d.out_w - io.out_shift);
     c.k_base = u * d.K_u + v * d.K_v + w * d.K_w;
     c.al = (uint32_t)d.a_c + (uint32_t)u * (uint32_t)d.a_u + (uint32_t)v * (uint32_t)d.a_v + (uint32_t)w * (uint32_t)d.a_w;
     c.be = (uint32_t)d.b_c + (uint32_t)u * (uint32_t)d.b_u + (uint32_t)v * (uint32_t)d.b_v + (uint32_t)w * (uint32_t)d.b_w;

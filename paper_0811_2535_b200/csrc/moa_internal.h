@@ -56,6 +56,10 @@ struct PassDesc {
     // NVLink-mapped; peer_off = this rank's source block); NULL peer[0] = send buffer
     double2 *peer[16];
     int64_t peer_off;
+    // batched transforms: tile id = bi * 2^ltiles + tile-in-transform; transform bi is
+    // offset by bi * bstride elements in src and dst (bstride 0 = no batch)
+    int ltiles;
+    int64_t bstride;
 };
 
 // L2-fused last two passes (persistent kernel): the middle pass of a 3-level

@@ -184,6 +184,7 @@ using namespace moa;
 
 struct moa_fft_plan_s {
     int64_t n = 0, M = 0;
+    int64_t batch = 1;   // independent transforms per execute (p == 1)
     int t = 0, p = 1, rank = 0, sign = -1, mode = MOA_MODE_LIFTED;
     int d = 0;
     int64_t lift[4] = {0, 0, 0, 0};
@@ -455,6 +456,24 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
                 D.out_k = D.K_k / P;
             }
         }
+        if (pl->batch > 1) {
+            if (d == 1) {
+                // tiles of T whole transforms (rows of n elements), one tile per group of T
+                int T = choose_T(pp.logF, pl->batch & -pl->batch);
+                pp.T = T;
+                D.in_t = pl->n;
+                D.out_t = pl->n;
+                D.out_tfast = 0;
+                D.ltiles = 0;
+                D.bstride = (int64_t)T * pl->n;
+                pp.tiles = pl->batch / T;
+            } else {
+                int lt = ilog2(pp.tiles);
+                D.ltiles = lt;
+                D.bstride = pl->n;
+                pp.tiles *= pl->batch;
+            }
+        }
         if (!pow2(D.U) || !pow2(D.V))
             return fail(MOA_ERR_INVALID_ARG, "internal: tile grid %lld x %lld not powers of two", (long long)D.U,
                         (long long)D.V);
@@ -621,6 +640,12 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     if (mode == MOA_MODE_LITERAL && p != 1)
         return fail(MOA_ERR_INVALID_P, "literal mode is single-GPU (p must be 1, got %d)", p);
     if (mode == MOA_MODE_EMULATED && p < 2) return fail(MOA_ERR_INVALID_P, "emulated mode needs p >= 2");
+    const int64_t batch = (opt && opt->batch > 1) ? opt->batch : 1;
+    if (opt && opt->batch < 0) return fail(MOA_ERR_INVALID_ARG, "batch %lld < 0", (long long)opt->batch);
+    if (batch > 1 && (p != 1 || mode != MOA_MODE_LIFTED))
+        return fail(MOA_ERR_INVALID_ARG, "batch > 1 needs p == 1 and the lifted mode");
+    if (batch > 1 && (double)batch * (double)n > 8.0 * (double)((int64_t)1 << 32))
+        return fail(MOA_ERR_INVALID_ARG, "batch * n = %.3g elements is beyond one GPU", (double)batch * n);
     const int exchange = (p > 1 && opt) ? opt->exchange : MOA_XCHG_NCCL;
     if (exchange < MOA_XCHG_NCCL || exchange > MOA_XCHG_P2P_EXTERNAL)
         return fail(MOA_ERR_INVALID_ARG, "unknown exchange %d", exchange);
@@ -645,6 +670,7 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     pl->rank = rank;
     pl->sign = sign;
     pl->mode = mode;
+    pl->batch = batch;
     pl->exchange = exchange;
     pl->M = n / p;
     CUDA_TRY(cudaGetDevice(&pl->device));
@@ -697,7 +723,7 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     if (mode == MOA_MODE_LITERAL) {
         pl->work_elems = n;
     } else {
-        pl->work_elems = pl->d > 1 ? pl->M : 0;
+        pl->work_elems = pl->d > 1 ? pl->M * pl->batch : 0;
         if (p > 1) pl->send_elems = (mode == MOA_MODE_EMULATED) ? n : pl->M;
     }
     // P2P: no send buffer; real ranks double-buffer the receive buffer (one barrier per execute)
@@ -722,8 +748,9 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
             free_plan(pl);
             return rc;
         }
-        for (auto &pp : pl->passes) choose_tma(pp);
-        const int fuse = env_int("MOA_FFT_FUSE", 0);
+        if (batch == 1)
+            for (auto &pp : pl->passes) choose_tma(pp);
+        const int fuse = batch == 1 ? env_int("MOA_FFT_FUSE", 0) : 0;
         if (p == 1 && pl->d == 3 && fuse && (rc = setup_fused(pl, fuse)) != MOA_OK) {
             free_plan(pl);
             return rc;
@@ -785,7 +812,7 @@ static int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *s
     snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : ""),
              1 << pp.logF, pp.T,
              peers ? "+push" : "");
-    ProfScope ps_(pl, name, 32 * pl->M);
+    ProfScope ps_(pl, name, 32 * pl->M * pl->batch);
     cudaError_t e;
     if (pp.tma && !peers) {
         if (pp.map_base != (const void *)src) {
@@ -956,7 +983,7 @@ int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
 int moa_fft_execute_host(moa_fft_plan_t pl, const void *host_in, void *host_out) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
     if (!host_in || !host_out) return fail(MOA_ERR_ALIGN, "NULL host buffer");
-    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M;
+    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M * pl->batch;
     size_t bytes = (size_t)elems * sizeof(double2);
     if (!pl->stage_in) {
         if (cudaMalloc((void **)&pl->stage_in, bytes) != cudaSuccess ||
@@ -990,7 +1017,7 @@ int moa_fft_execute_host_batch(moa_fft_plan_t pl, int count, const void *const *
             if (cur != dev) cudaSetDevice(cur);
         }
     } restore_{cur, pl->device};
-    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M;
+    int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M * pl->batch;
     size_t bytes = (size_t)elems * sizeof(double2);
     if (!pl->stage_in) {
         if (cudaMalloc((void **)&pl->stage_in, bytes) != cudaSuccess ||
@@ -1165,7 +1192,7 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
         o->hbm_bytes = 32 * pl->n * (pl->t + 1);
     } else if (pl->p == 1) {
         o->launches = pl->fused ? pl->d - 1 : pl->d;
-        o->hbm_bytes = 32 * pl->n * (pl->fused ? pl->d - 1 : pl->d);
+        o->hbm_bytes = 32 * pl->n * pl->batch * (pl->fused ? pl->d - 1 : pl->d);
     } else {
         int per_rank = pl->d + 1;
         o->launches = pl->mode == MOA_MODE_EMULATED ? pl->p * per_rank : per_rank;
@@ -1173,6 +1200,7 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
         o->a2a_bytes = 16 * pl->M / pl->p * (pl->p - 1) * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
     }
     o->workspace_bytes = pl->workspace_bytes;
+    o->batch = pl->batch;
     return MOA_OK;
 }
 

@@ -78,3 +78,27 @@ def test_dist_plan_without_init_is_rejected():
     h = lib.moa_fft_plan(1 << 10, 2, -1)
     assert not h
     assert "moa_dist_init" in lib.moa_fft_last_error().decode()
+
+
+@pytest.mark.parametrize("kw,needle", [
+    ({"p": 2, "batch": 4, "mode": moa.MODE_EMULATED}, "batch > 1 needs p == 1"),
+    ({"batch": 4, "mode": moa.MODE_LITERAL}, "batch > 1 needs p == 1"),
+    ({"batch": -3}, "batch -3 < 0"),
+    ({"p": 2, "exchange": 7, "mode": moa.MODE_EMULATED}, "unknown exchange"),
+    ({"p": 2, "exchange": moa.XCHG_P2P_EXTERNAL, "rank": 5}, "rank 5 outside"),
+])
+def test_option_validation_errors(kw, needle):
+    """Option checks run before any device call (CPU-testable)."""
+    p = kw.pop("p", 1)
+    with pytest.raises(moa.MoaError) as e:
+        moa.Plan(1 << 10, p, -1, **kw)
+    assert needle in str(e.value), str(e.value)
+
+
+def test_p2p_calls_reject_non_p2p_plans():
+    lib = moa.load()
+    assert lib.moa_fft_ipc_handle(None, None) == -9
+    assert lib.moa_fft_ipc_open(None, None) == -9
+    assert lib.moa_fft_enable_p2p(None) == -9
+    assert lib.moa_fft_execute_phase(None, None, None, 1) == -9
+    assert lib.moa_fft_execute_host_batch(None, 0, None, None) == -9

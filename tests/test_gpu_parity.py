@@ -164,6 +164,32 @@ def test_variant_kernels_parity(env, monkeypatch):
             assert oracle.rel_l2(got, ref) <= tol(t), (env, t)
 
 
+@pytest.mark.parametrize("t,batch", [(1, 5), (3, 64), (8, 3), (10, 96), (12, 7), (13, 2), (16, 12), (20, 3),
+                                     (22, 2)])
+def test_batched_transforms(t, batch):
+    """`batch` independent transforms back to back in one execute (one
+    launch per pass for the whole batch) -- each equals the single-transform oracle."""
+    n = 1 << t
+    xs = [moa_inputs.complex_signal(moa_inputs.seed_for(t) + 17 * b, n) for b in range(batch)]
+    plan = moa.Plan(n, batch=batch)
+    assert plan.info()["batch"] == batch
+    for sign in (-1, 1):
+        plan_s = plan if sign == -1 else moa.Plan(n, 1, sign, batch=batch)
+        got = _run(plan_s, np.concatenate(xs)).reshape(batch, n)
+        for b in range(batch):
+            assert oracle.rel_l2(got[b], oracle.fft(xs[b], sign, threads=8)) <= tol(max(t, 1)), (t, batch, b, sign)
+
+
+def test_batched_equals_single_bitwise():
+    t, batch = 14, 6
+    n = 1 << t
+    x = np.concatenate([moa_inputs.complex_signal(moa_inputs.seed_for(t) + b, n) for b in range(batch)])
+    got = _run(moa.Plan(n, batch=batch), x).reshape(batch, n)
+    single = moa.Plan(n)
+    for b in range(batch):
+        assert np.array_equal(got[b], _run(single, x[b * n:(b + 1) * n]))
+
+
 def test_misaligned_pointer_rejected():
     x = torch.zeros(1 << 10 + 1, dtype=torch.complex128, device="cuda")
     plan = moa.Plan(1 << 10)
