@@ -117,6 +117,18 @@ typedef struct {
  */
 moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign);
 
+/*
+ * Two-dimensional transform: App. B's Omega applies a 1-D
+ * operation to every sub-array along an axis (B.1-B.6), so the 2-D DFT
+ *   X[k1][k2] = sum_{j1,j2} x[j1][j2] exp(sign*2*pi*i*(j1*k1/n1 + j2*k2/n2))
+ * is the lifted 1-D FFT over the rows followed by the same over the columns.
+ *   n1 = 2^t1, 1 <= t1 <= 13 (the column transforms are one pass), n2 = 2^t2 with
+ *   t2 >= 1 (the rows are a batched lifted 1-D plan), n1 * n2 <= 2^32.
+ * x, X: n1 x n2 complex128, row-major (element (j1, j2) at j1*n2 + j2).  Execute
+ * with moa_fft_execute; in == out allowed.  NULL on error (moa_fft_last_error).
+ */
+moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign);
+
 /* As moa_fft_plan with explicit options (NULL = defaults).  A lifting whose
  * product is wrong or with a factor outside [2, 8192] is MOA_ERR_INVALID_ARG. */
 moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options *opts);

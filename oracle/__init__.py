@@ -17,6 +17,9 @@ paper figure it follows (P:<line> of PAPER.md, arXiv 0811.2535):
 * ``weights``   -- weight(row) = EXP(sign 2 pi i row / L) (Fig 3.8)
 * ``dist_sim``  -- Fig 5.7 + Fig 5.9 with m virtual processors
 * ``gamma``     -- row-major offset, Def A.1
+* ``fft2``      -- 2-D DFT as App. B's Omega: (fft Omega <1>) over the rows, transpose
+                   (Fig A.1), (fft Omega <1>) again, transpose back (B.1-B.6)
+* ``dft2``      -- the plain 2-D definition, O((n1 n2)^2), for pinning ``fft2``
 """
 from __future__ import annotations
 
@@ -192,3 +195,42 @@ def rel_l2(got, ref) -> float:
     """relL2 = ||g - o||_2 / ||o||_2 accumulated in long double."""
     num, den = l2_parts(got, ref)
     return float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num))
+
+
+def fft2(x, sign: int = -1, threads: int = 1) -> np.ndarray:
+    """2-D DFT of an n1 x n2 array via App. B's Omega.
+
+    (f Omega <1>) xi applies f to every 1-D sub-array i psi xi along the last axis
+    (B.4-B.6): step 1 the rows, step 2 the transpose of Fig A.1, step 3 the rows of
+    the transpose (= the columns), step 4 the transpose back.  f = ``fft`` (Fig 3.9)."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    if a.ndim != 2:
+        raise ValueError("fft2 expects a 2-D array")
+    y = np.stack([fft(row, sign, threads) for row in a])            # (fft Omega <1>) x
+    z = np.ascontiguousarray(y.T)                                    # transpose
+    w = np.stack([fft(row, sign, threads) for row in z])            # (fft Omega <1>) z
+    return np.ascontiguousarray(w.T)                                 # transpose back
+
+
+def dft2(x, sign: int = -1) -> np.ndarray:
+    """X[k1,k2] = sum_{j1,j2} x[j1,j2] exp(sign 2 pi i (j1 k1/n1 + j2 k2/n2)), written out
+    as the double sum in long double with exactly reduced exponents (tiny arrays only)."""
+    a = np.asarray(x, dtype=np.complex128)
+    n1, n2 = a.shape
+    out = np.empty((n1, n2), dtype=np.complex128)
+    ld = np.longdouble
+    for k1 in range(n1):
+        for k2 in range(n2):
+            re = ld(0)
+            im = ld(0)
+            for j1 in range(n1):
+                for j2 in range(n2):
+                    # angle as an exact fraction of a turn: (j1 k1 n2 + j2 k2 n1) / (n1 n2)
+                    e = (j1 * k1 * n2 + j2 * k2 * n1) % (n1 * n2)
+                    th = ld(sign) * ld(2) * ld(np.pi) * ld(e) / ld(n1 * n2)
+                    c, s_ = np.cos(th), np.sin(th)
+                    xr, xi = ld(a[j1, j2].real), ld(a[j1, j2].imag)
+                    re += xr * c - xi * s_
+                    im += xr * s_ + xi * c
+            out[k1, k2] = complex(float(re), float(im))
+    return out

@@ -17,7 +17,7 @@ import os
 
 from . import build as _build
 
-__all__ = ["Plan", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
+__all__ = ["Plan", "Plan2D", "fft2", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
            "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
@@ -56,7 +56,8 @@ EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execut
            "moa_fft_destroy", "moa_fft_set_stream", "moa_fft_plan_info", "moa_fft_last_error",
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
-           "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase"]
+           "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase",
+           "moa_fft_plan_2d"]
 
 _lib = None
 
@@ -80,6 +81,8 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_plan.restype = vp
     lib.moa_fft_plan_ex.argtypes = [i64, ci, ci, ctypes.POINTER(_Options)]
     lib.moa_fft_plan_ex.restype = vp
+    lib.moa_fft_plan_2d.argtypes = [i64, i64, ci]
+    lib.moa_fft_plan_2d.restype = vp
     lib.moa_fft_execute.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host_batch.argtypes = [vp, ci, vp, vp]
@@ -267,6 +270,37 @@ class Plan:
             self.destroy()
         except Exception:
             pass
+
+
+class Plan2D(Plan):
+    """2-D transform of an n1 x n2 row-major complex128 array (moa_fft_plan_2d): the lifted
+    1-D FFT over the rows, then one pass of n1-point DFTs over the columns (App. B's Omega)."""
+
+    def __init__(self, n1: int, n2: int, sign: int = -1, stream=None):
+        lib = load()
+        h = lib.moa_fft_plan_2d(int(n1), int(n2), int(sign))
+        if not h:
+            raise MoaError(-9, lib.moa_fft_last_error().decode())
+        self._h = h
+        self.n1, self.n2 = int(n1), int(n2)
+        self.n, self.p, self.sign, self.mode = self.n1 * self.n2, 1, int(sign), MODE_LIFTED
+        self.exchange, self.rank, self.batch = XCHG_NCCL, 0, 1
+        self._stream = None
+        self.set_stream(stream)
+
+
+def fft2(x, sign: int = -1, out=None):
+    """2-D transform of a 2-D complex128 CUDA tensor (rows contiguous)."""
+    import torch
+    if x.dtype != torch.complex128 or not x.is_cuda or x.dim() != 2:
+        raise ValueError("fft2 expects a 2-D complex128 CUDA tensor")
+    x = x.contiguous()
+    plan = Plan2D(x.shape[0], x.shape[1], sign)
+    try:
+        return plan.execute(x, out)
+    finally:
+        torch.cuda.current_stream().synchronize()
+        plan.destroy()
 
 
 def fft(x, sign: int = -1, out=None):

@@ -329,6 +329,55 @@ __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 
     }
 }
 
+// Early-issued pass-twiddle operands (MOA_PTW_EARLY): the two-level table loads of the
+// (at most EPT) entries this thread builds are issued BEFORE the tile's input loads, so
+// they return (L2 hits) while the inputs are still in flight; the products and stores
+// into the tile tables happen after the input gather.
+#ifndef MOA_PTW_EARLY
+#define MOA_PTW_EARLY 0
+#endif
+#ifndef MOA_CONJ_LOP
+#define MOA_CONJ_LOP 0
+#endif
+template <int F, int T>
+struct TwEarly {
+    using SH = PassShape<F, T>;
+    static constexpr int ENT = T * (SH::LNB + SH::LRS);
+    static constexpr int EPT = (ENT + SH::NT - 1) / SH::NT;
+    double2 hi[EPT], lo[EPT];
+    __device__ __forceinline__ void issue(const PassDesc &d, uint32_t al, uint32_t be) {
+        constexpr int NB = SH::LNB, RS = SH::LRS;
+        const uint32_t nm = (uint32_t)d.nmask;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int i = threadIdx.x + q * SH::NT;
+            uint32_t e = 0;
+            if (i < T * NB) {
+                const int t = i / NB, j = i % NB;
+                e = (al + (uint32_t)t * (uint32_t)d.a_t + (be + (uint32_t)t * (uint32_t)d.b_t) * (uint32_t)j) & nm;
+            } else if (i < ENT) {
+                const int k = i - T * NB, t = k / RS, r = k % RS;
+                e = ((be + (uint32_t)t * (uint32_t)d.b_t) * (uint32_t)(NB * r)) & nm;
+            }
+            hi[q] = __ldg(d.tw_hi + (e >> d.hbits));
+            lo[q] = __ldg(d.tw_lo + (e & ((1u << d.hbits) - 1)));
+        }
+    }
+    __device__ __forceinline__ void finish(double2 *twa, double2 *twb) const {
+        constexpr int NB = SH::LNB, RS = SH::LRS;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int i = threadIdx.x + q * SH::NT;
+            if (i < T * NB) {
+                twa[(i / NB) * (NB + 1) + i % NB] = cmul(hi[q], lo[q]);
+            } else if (i < ENT) {
+                const int k = i - T * NB;
+                twb[(k / RS) * (RS + 1) + k % RS] = cmul(hi[q], lo[q]);
+            }
+        }
+    }
+};
+
 // One Stockham stage: Ns = product of the radices already applied.
 //   SRC 0: the first stage gathers from global memory; SRC 1/2: from the TMA
 //   staging buffer `inbuf`, after which hook() runs (barrier + next prefetch).
@@ -372,6 +421,10 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     // ---- gather inputs (the first stage then builds the tile's twiddle tables while
     //      its loads are in flight)
     if constexpr (FIRST && SRC == 0) {
+#if MOA_PTW_EARLY
+        TwEarly<F, T> twe;
+        if (d.twiddle) twe.issue(d, c.al, c.be);
+#endif
         // element offsets inside the tile's span fit 32 bits (span < n <= 2^32)
         const uint32_t sf = (uint32_t)NB * (uint32_t)d.in_f;
 #pragma unroll
@@ -380,11 +433,23 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int r = 0; r < RS; ++r) x[i * RS + r] = ld_io<LD>(elem_off_c(p, r, sf), pol);
         }
+#if MOA_CONJ_LOP
+        {   // sign flip of the imaginary parts on the integer pipe (mask 0 for sign -1)
+            const unsigned cm = d.conj_in ? 0x80000000u : 0u;
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k] = conj_mask(x[k], cm);
+        }
+#else
         if (d.conj_in) {
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
+#endif
+#if MOA_PTW_EARLY
+        if (d.twiddle) twe.finish(const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb));
+#else
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+#endif
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
     } else if constexpr (FIRST && SRC == 3) {
         // prefetched by this same thread (cp.async, fft_pass_pf_kernel) into the
@@ -465,10 +530,18 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
                 for (int r = 1; r < RS; ++r) v[r] = cmul(v[r], cmul(a, c.twb[t * (RS + 1) + r]));
             }
+#if MOA_CONJ_LOP
+            {
+                const unsigned cm = d.conj_out ? 0x80000000u : 0u;
+#pragma unroll
+                for (int r = 0; r < RS; ++r) v[r] = conj_mask(v[r], cm);
+            }
+#else
             if (d.conj_out) {
 #pragma unroll
                 for (int r = 0; r < RS; ++r) v[r].y = -v[r].y;
             }
+#endif
             if (d.pack_lp >= 0) {   // general pack (single-level local transform, p > 1)
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {

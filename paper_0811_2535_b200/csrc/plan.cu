@@ -185,6 +185,10 @@ using namespace moa;
 struct moa_fft_plan_s {
     int64_t n = 0, M = 0;
     int64_t batch = 1;   // independent transforms per execute (p == 1)
+    // 2-D plans (moa_fft_plan_2d): rows = batched 1-D plan of length n2, col = one pass
+    // of n1-point DFTs along the stride-n2 axis, in place on the output
+    int64_t n1 = 0, n2 = 0;
+    moa_fft_plan_s *rows = nullptr;
     int t = 0, p = 1, rank = 0, sign = -1, mode = MOA_MODE_LIFTED;
     int d = 0;
     int64_t lift[4] = {0, 0, 0, 0};
@@ -207,7 +211,7 @@ struct moa_fft_plan_s {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
     int64_t work_elems = 0, send_elems = 0;
-    std::vector<PassPlan> passes;   // p == 1: all passes; p > 1: phase 1 for rank `rank`
+    std::vector<PassPlan> passes;   // p == 1: all passes; p > 1: phase 1 for rank `rank`; 2-D: the column pass
     std::vector<std::vector<PassPlan>> rank_passes;  // emulated: phase 1 per virtual rank
     int64_t workspace_bytes = 0;
     // L2-fused last two passes (fused.cu)
@@ -488,6 +492,10 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
 
 static void free_plan(moa_fft_plan_s *pl) {
     if (!pl) return;
+    if (pl->rows) {
+        free_plan(pl->rows);
+        pl->rows = nullptr;
+    }
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(pl->device);
@@ -760,6 +768,73 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     return MOA_OK;
 }
 
+// 2-D transform of an n1 x n2 row-major array: App. B's Omega
+// applies a 1-D operation to every sub-array along an axis (B.1-B.6);
+// the 2-D DFT is (FFT Omega <1>) over the rows followed by the same over the columns.
+// Rows: a batched lifted 1-D plan (batch n1, length n2).  Columns: one pass of
+// n1-point DFTs along the stride-n2 axis -- the middle-pass tile of §4 with the view
+// [1][n1][n2], no twiddle, in place -- so n1 <= FMAX.
+static int make_plan_2d(int64_t n1, int64_t n2, int sign, moa_fft_plan_s **res) {
+    *res = nullptr;
+    if (!pow2(n1) || n1 < 2 || n1 > FMAX)
+        return fail(MOA_ERR_INVALID_N, "n1=%lld must be 2^t1 with 1 <= t1 <= %d (one column pass)", (long long)n1,
+                    FMAX_LOG);
+    if (!pow2(n2) || n2 < 2 || n1 * n2 > ((int64_t)1 << 32))
+        return fail(MOA_ERR_INVALID_N, "n2=%lld must be 2^t2, t2 >= 1, with n1*n2 <= 2^32", (long long)n2);
+    if (sign != -1 && sign != 1) return fail(MOA_ERR_INVALID_SIGN, "sign=%d must be -1 or +1", sign);
+    moa_fft_options o;
+    memset(&o, 0, sizeof o);
+    o.mode = MOA_MODE_LIFTED;
+    o.batch = n1;
+    moa_fft_plan_s *rows = nullptr;
+    int rc = make_plan(n2, 1, sign, &o, &rows);
+    if (rc) return rc;
+    moa_fft_plan_s *pl = new moa_fft_plan_s();
+    pl->rows = rows;
+    pl->n1 = n1;
+    pl->n2 = n2;
+    pl->n = n1 * n2;
+    pl->M = pl->n;
+    pl->t = ilog2(pl->n);
+    pl->sign = sign;
+    pl->device = rows->device;
+    pl->d = 1;
+    pl->lift[0] = n1;
+    PassPlan pp;
+    memset(&pp.d, 0, sizeof(PassDesc));
+    PassDesc &D = pp.d;
+    pp.logF = ilog2(n1);
+    pp.T = choose_T(pp.logF, n2);
+    D.nmask = (uint64_t)n1 - 1;
+    D.hbits = rows->hbits;
+    D.tbits = pp.logF;
+    D.tw_hi = rows->tw_hi;
+    D.tw_lo = rows->tw_lo;
+    D.tw_f = rows->tw_f;
+    D.pack_lp = -1;
+    D.conj_in = D.conj_out = sign > 0;   // conj(DFT_-1(conj y)) along the columns
+    D.U = n2 / pp.T;
+    D.V = 1;
+    D.lU = ilog2(D.U);
+    D.lV = 0;
+    D.in_u = pp.T;
+    D.in_t = 1;
+    D.in_f = n2;
+    D.in_tfast = D.out_tfast = pp.T > 1;
+    D.out_u = D.in_u;
+    D.out_t = D.in_t;
+    D.out_k = D.in_f;
+    pp.tiles = D.U;
+    if (!pass_supported(pp.logF, pp.T)) {
+        free_plan(pl);
+        return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
+    }
+    pl->passes.push_back(pp);
+    pl->stream = rows->stream;
+    *res = pl;
+    return MOA_OK;
+}
+
 static bool aligned16(const void *ptr) { return ptr && ((uintptr_t)ptr & 15) == 0; }
 
 // ---- event profiling: a scope records an event pair around one launch
@@ -862,6 +937,13 @@ static int p2p_phase(moa_fft_plan_s *pl, const double2 *in, double2 *out, int ph
 
 static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
     cudaStream_t s = pl->stream;
+    if (pl->rows) {   // 2-D: (FFT Omega <1>) over the rows, then the column pass in place
+        pl->rows->stream = s;
+        pl->rows->profiling = pl->profiling;
+        int rc = execute(pl->rows, in, out);
+        if (rc) return rc;
+        return launch_pp(pl, pl->passes[0], 1, out, out);
+    }
     if (pl->mode == MOA_MODE_LITERAL) {
         // Fig 2.1 literally: (1) x <- P_n x; (2)-(7) t radix-2 stages (Fig 3.9)
         const int t = pl->t;
@@ -967,6 +1049,13 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
 }
 
 moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign) { return moa_fft_plan_ex(n, p, sign, nullptr); }
+
+moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign) {
+    g_err.clear();
+    moa_fft_plan_s *pl = nullptr;
+    if (make_plan_2d(n1, n2, sign, &pl) != MOA_OK) return nullptr;
+    return pl;
+}
 
 int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
@@ -1170,6 +1259,7 @@ int moa_fft_execute_phase(moa_fft_plan_t pl, const void *in, void *out, int phas
 int moa_fft_set_stream(moa_fft_plan_t pl, void *stream) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
     pl->stream = (cudaStream_t)stream;
+    if (pl->rows) pl->rows->stream = pl->stream;
     return MOA_OK;
 }
 
@@ -1201,6 +1291,14 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
     }
     o->workspace_bytes = pl->workspace_bytes;
     o->batch = pl->batch;
+    if (pl->rows) {   // 2-D: the row plan's passes, then the column pass
+        o->passes = pl->rows->d + 1;
+        for (int i = 0; i < 4; ++i) o->lift[i] = i < pl->rows->d ? pl->rows->lift[i] : (i == pl->rows->d ? pl->n1 : 0);
+        o->launches = pl->rows->d + 1;
+        o->hbm_bytes = 32 * pl->n * (pl->rows->d + 1);
+        o->workspace_bytes = pl->rows->workspace_bytes;
+        o->batch = 1;
+    }
     return MOA_OK;
 }
 
@@ -1269,6 +1367,27 @@ int moa_fft_set_profiling(moa_fft_plan_t pl, int enable) {
 
 int moa_fft_get_profile(moa_fft_plan_t pl, moa_fft_kernel_stat *stats, int max_stats) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
+    if (pl->rows) {   // 2-D: the row plan's kernels first (prefixed "rows "), then the column pass
+        pl->rows->stream = pl->stream;
+        int k = moa_fft_get_profile(pl->rows, stats, max_stats);
+        if (k < 0) return k;
+        for (int i = 0; i < k; ++i) {
+            char tmp[64];
+            snprintf(tmp, sizeof tmp, "rows %s", stats[i].name);
+            memcpy(stats[i].name, tmp, sizeof tmp);
+        }
+        moa_fft_plan_s *rows = pl->rows;
+        pl->rows = nullptr;   // collect this plan's own slots
+        int k2 = moa_fft_get_profile(pl, stats ? stats + k : nullptr, max_stats - k);
+        pl->rows = rows;
+        if (k2 < 0) return k2;
+        for (int i = k; i < k + k2; ++i) {
+            char tmp[64];
+            snprintf(tmp, sizeof tmp, "cols %s", stats[i].name);
+            memcpy(stats[i].name, tmp, sizeof tmp);
+        }
+        return k + k2;
+    }
     CUDA_TRY(cudaStreamSynchronize(pl->stream));
     for (auto &sl : pl->slots) {
         sl.launches = 0;

@@ -190,6 +190,26 @@ def test_batched_equals_single_bitwise():
         assert np.array_equal(got[b], _run(single, x[b * n:(b + 1) * n]))
 
 
+@pytest.mark.parametrize("n1,n2", [(2, 2), (16, 8), (8, 4096), (256, 256), (64, 1 << 14), (1024, 512),
+                                   (8192, 16), (2, 1 << 20)])
+def test_2d_transform(n1, n2):
+    """2-D DFT via Omega (App. B) against oracle.fft2 (pinned by the
+    double sum), both signs."""
+    x = moa_inputs.complex_signal(0x2D00 + n1 + n2, n1 * n2).reshape(n1, n2)
+    for sign in (-1, 1):
+        got = _run(moa.Plan2D(n1, n2, sign), x.reshape(-1)).reshape(n1, n2)
+        ref = oracle.fft2(x, sign, threads=8)
+        t = (n1 * n2).bit_length() - 1
+        assert oracle.rel_l2(got, ref) <= tol(t), (n1, n2, sign)
+
+
+def test_2d_rejects_bad_shapes():
+    with pytest.raises(moa.MoaError):
+        moa.Plan2D(1 << 14, 4)
+    with pytest.raises(moa.MoaError):
+        moa.Plan2D(12, 16)
+
+
 def test_misaligned_pointer_rejected():
     x = torch.zeros(1 << 10 + 1, dtype=torch.complex128, device="cuda")
     plan = moa.Plan(1 << 10)

@@ -323,3 +323,31 @@ def test_rejects_invalid_n():
         oracle.fft(np.zeros(6, complex))
     with pytest.raises(ValueError):
         oracle.fft(np.zeros(1, complex))  # t >= 1
+
+
+# ------------------------------------------------------------------ 2-D via Omega (App. B)
+@pytest.mark.parametrize("n1,n2", [(2, 2), (2, 8), (4, 4), (8, 2), (4, 16)])
+def test_fft2_equals_bruteforce_double_sum(n1, n2):
+    """fft2 (rows, transpose, rows, transpose) against the 2-D definition written out."""
+    x = moa_inputs.complex_signal(0x2D2D + n1 * 131 + n2, n1 * n2).reshape(n1, n2)
+    for sign in (-1, 1):
+        assert oracle.rel_l2(oracle.fft2(x, sign), oracle.dft2(x, sign)) <= 1e-14
+
+
+def test_fft2_separable_closed_form():
+    """x = a (outer) b  =>  X = A (outer) B with A, B the 1-D transforms (closed form of
+    the separable sum); a 2-D impulse goes to all ones, bitwise."""
+    n1, n2 = 32, 64
+    a = moa_inputs.complex_signal(11, n1)
+    b = moa_inputs.complex_signal(12, n2)
+    X = oracle.fft2(np.outer(a, b))
+    assert oracle.rel_l2(X, np.outer(oracle.fft(a), oracle.fft(b))) <= 1e-14
+    d = np.zeros((n1, n2), complex)
+    d[0, 0] = 1
+    assert np.array_equal(oracle.fft2(d), np.ones((n1, n2), complex))
+
+
+def test_fft2_library_special_case():
+    x = moa_inputs.complex_signal(0x2D, 64 * 128).reshape(64, 128)
+    assert oracle.rel_l2(oracle.fft2(x, -1), np.fft.fft2(x)) <= 1e-14
+    assert oracle.rel_l2(oracle.fft2(x, +1), np.fft.ifft2(x) * x.size) <= 1e-14
