@@ -604,6 +604,11 @@ template <int F, int T>
 __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     fft_pass_kernel(const PassDesc d) {
     extern __shared__ double2 sm[];
+    if (d.pdl) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    if (d.stagger_ns && blockIdx.x < 4u * d.stagger_sms) __nanosleep((blockIdx.x / d.stagger_sms) * d.stagger_ns);
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     tile_fft<F, T>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
                    blockIdx.x);
@@ -725,6 +730,19 @@ int grid_one_pf() {
 template <int F, int T>
 cudaError_t launch_one(const PassDesc &d, int64_t tiles, cudaStream_t s) {
     using SH = PassShape<F, T>;
+    if (d.pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)tiles);
+        cfg.blockDim = dim3(SH::NT);
+        cfg.dynamicSmemBytes = SH::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fft_pass_kernel<F, T>, d);
+    }
     fft_pass_kernel<F, T><<<(unsigned)tiles, SH::NT, SH::SMEM, s>>>(d);
     return cudaGetLastError();
 }

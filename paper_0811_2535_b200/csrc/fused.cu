@@ -20,6 +20,10 @@
 // whatever the residency.  Counters are monotone across executes (epoch).
 #include "fft_pass.cuh"
 
+#ifndef MOA_FUSE_ACQ
+#define MOA_FUSE_ACQ 1
+#endif
+
 namespace moa {
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
@@ -34,6 +38,12 @@ __device__ __forceinline__ void red_release_add(unsigned long long *p, unsigned 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void wait_geq(const unsigned long long *p, unsigned long long target) {
     if (ld_acquire_u64(p) >= target) return;
     unsigned ns = 32;
@@ -41,6 +51,23 @@ __device__ __forceinline__ void wait_geq(const unsigned long long *p, unsigned l
         __nanosleep(ns);
         if (ns < 512) ns <<= 1;
     }
+}
+
+// Ticket-kernel wait: poll relaxed (an acquire load compiles to an L1 invalidation,
+// CCTL.IVALL, which would evict the twiddle tables of every CTA on the SM), then one
+// acquire once the target is reached.  The consumer reads the producer's data with
+// ld.global.cg (L2) only.
+__device__ __forceinline__ void wait_geq_relaxed(const unsigned long long *p, unsigned long long target) {
+    if (ld_relaxed_u64(p) < target) {
+        unsigned ns = 32;
+        while (ld_relaxed_u64(p) < target) {
+            __nanosleep(ns);
+            if (ns < 512) ns <<= 1;
+        }
+    }
+#if MOA_FUSE_ACQ
+    (void)ld_acquire_u64(p);
+#endif
 }
 
 template <int F2, int T2, int F3, int T3>
@@ -206,8 +233,9 @@ __global__ void __launch_bounds__(TicketShape<F2, T2, F3, T3>::NT, TicketShape<F
             fd.ticket == 2 ? atomicAdd(fd.claim, 1ull) - fd.epoch * (unsigned long long)fd.total_items : blockIdx.x;
         const int code = __ldg(fd.items + ticket);
         const int kind = code >> 30, g = (code >> 16) & 0x3fff;
-        if (kind == 1) wait_geq(fd.done2 + g, (fd.epoch + 1) * (unsigned long long)fd.tiles2);
-        else if (g >= fd.slots) wait_geq(fd.done3 + (g - fd.slots), (fd.epoch + 1) * (unsigned long long)fd.tiles3);
+        if (kind == 1) wait_geq_relaxed(fd.done2 + g, (fd.epoch + 1) * (unsigned long long)fd.tiles2);
+        else if (g >= fd.slots)
+            wait_geq_relaxed(fd.done3 + (g - fd.slots), (fd.epoch + 1) * (unsigned long long)fd.tiles3);
         s_code = code;
     }
     __syncthreads();
