@@ -129,6 +129,17 @@ moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign);
  */
 moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign);
 
+/*
+ * r-dimensional transform, r = 2 or 3, of a row-major shape[0] x ... x shape[r-1]
+ * complex128 array: X[k] = sum_j x[j] exp(sign*2*pi*i * sum_a j_a*k_a/shape[a]).
+ * The last axis is any power of two (a batched lifted 1-D plan); every other axis is
+ * 2^t with 1 <= t <= 13 (one pass of DFTs along that strided axis, in place), in the
+ * order last-but-one axis first.  The product of the extents is <= 2^32.  Execute
+ * with moa_fft_execute; in == out allowed.  NULL on error.  (moa_fft_plan_2d is the
+ * rank-2 case.)
+ */
+moa_fft_plan_t moa_fft_plan_nd(int rank, const int64_t *shape, int sign);
+
 /* As moa_fft_plan with explicit options (NULL = defaults).  A lifting whose
  * product is wrong or with a factor outside [2, 8192] is MOA_ERR_INVALID_ARG. */
 moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options *opts);

@@ -20,6 +20,8 @@ paper figure it follows (P:<line> of PAPER.md, arXiv 0811.2535):
 * ``fft2``      -- 2-D DFT as App. B's Omega: (fft Omega <1>) over the rows, transpose
                    (Fig A.1), (fft Omega <1>) again, transpose back (B.1-B.6)
 * ``dft2``      -- the plain 2-D definition, O((n1 n2)^2), for pinning ``fft2``
+* ``fftn``      -- r-D DFT via Omega: ``fft`` along every axis in turn (last axis first)
+* ``dftn``      -- the plain r-D definition (tiny arrays), for pinning ``fftn``
 """
 from __future__ import annotations
 
@@ -233,4 +235,40 @@ def dft2(x, sign: int = -1) -> np.ndarray:
                     re += xr * c - xi * s_
                     im += xr * s_ + xi * c
             out[k1, k2] = complex(float(re), float(im))
+    return out
+
+
+def fftn(x, sign: int = -1, threads: int = 1) -> np.ndarray:
+    """r-D DFT via App. B's Omega: for each axis a (last first), move axis a last
+    (a transpose, Fig A.1), apply (fft Omega <1>) to every 1-D sub-array (B.4-B.6),
+    move it back.  f = ``fft`` (Fig 3.9)."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    for ax in range(a.ndim - 1, -1, -1):
+        m = np.ascontiguousarray(np.moveaxis(a, ax, -1))
+        flat = m.reshape(-1, m.shape[-1])
+        res = np.stack([fft(row, sign, threads) for row in flat]).reshape(m.shape)
+        a = np.ascontiguousarray(np.moveaxis(res, -1, ax))
+    return a
+
+
+def dftn(x, sign: int = -1) -> np.ndarray:
+    """The r-D definition written out as one sum over all index tuples (long double,
+    exponents reduced exactly modulo the array size); tiny arrays only."""
+    a = np.asarray(x, dtype=np.complex128)
+    shape = a.shape
+    N = int(np.prod(shape))
+    idx = list(np.ndindex(*shape))
+    out = np.empty(shape, dtype=np.complex128)
+    ld = np.longdouble
+    for k in idx:
+        re = ld(0)
+        im = ld(0)
+        for j in idx:
+            e = sum(j[d] * k[d] * (N // shape[d]) for d in range(len(shape))) % N
+            th = ld(sign) * ld(2) * ld(np.pi) * ld(e) / ld(N)
+            c, s_ = np.cos(th), np.sin(th)
+            xr, xi = ld(a[j].real), ld(a[j].imag)
+            re += xr * c - xi * s_
+            im += xr * s_ + xi * c
+        out[k] = complex(float(re), float(im))
     return out

@@ -17,7 +17,7 @@ import os
 
 from . import build as _build
 
-__all__ = ["Plan", "Plan2D", "fft2", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
+__all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
            "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
@@ -57,7 +57,7 @@ EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execut
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
            "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase",
-           "moa_fft_plan_2d"]
+           "moa_fft_plan_2d", "moa_fft_plan_nd"]
 
 _lib = None
 
@@ -83,6 +83,8 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_plan_ex.restype = vp
     lib.moa_fft_plan_2d.argtypes = [i64, i64, ci]
     lib.moa_fft_plan_2d.restype = vp
+    lib.moa_fft_plan_nd.argtypes = [ci, vp, ci]
+    lib.moa_fft_plan_nd.restype = vp
     lib.moa_fft_execute.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host_batch.argtypes = [vp, ci, vp, vp]
@@ -287,6 +289,41 @@ class Plan2D(Plan):
         self.exchange, self.rank, self.batch = XCHG_NCCL, 0, 1
         self._stream = None
         self.set_stream(stream)
+
+
+class PlanND(Plan):
+    """r-D transform (r = 2, 3) of a row-major complex128 array (moa_fft_plan_nd): the lifted
+    1-D FFT along the last axis, then one pass along each other axis (App. B's Omega)."""
+
+    def __init__(self, shape, sign: int = -1, stream=None):
+        lib = load()
+        shp = (ctypes.c_int64 * len(shape))(*[int(v) for v in shape])
+        h = lib.moa_fft_plan_nd(len(shape), shp, int(sign))
+        if not h:
+            raise MoaError(-9, lib.moa_fft_last_error().decode())
+        self._h = h
+        self.shape = tuple(int(v) for v in shape)
+        n = 1
+        for v in self.shape:
+            n *= v
+        self.n, self.p, self.sign, self.mode = n, 1, int(sign), MODE_LIFTED
+        self.exchange, self.rank, self.batch = XCHG_NCCL, 0, 1
+        self._stream = None
+        self.set_stream(stream)
+
+
+def fftn(x, sign: int = -1, out=None):
+    """2-D or 3-D transform of a complex128 CUDA tensor (row-major)."""
+    import torch
+    if x.dtype != torch.complex128 or not x.is_cuda or x.dim() not in (2, 3):
+        raise ValueError("fftn expects a 2-D or 3-D complex128 CUDA tensor")
+    x = x.contiguous()
+    plan = PlanND(tuple(x.shape), sign)
+    try:
+        return plan.execute(x, out)
+    finally:
+        torch.cuda.current_stream().synchronize()
+        plan.destroy()
 
 
 def fft2(x, sign: int = -1, out=None):

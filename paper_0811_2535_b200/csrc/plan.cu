@@ -776,68 +776,85 @@ static int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa
     return MOA_OK;
 }
 
-// 2-D transform of an n1 x n2 row-major array: App. B's Omega
-// applies a 1-D operation to every sub-array along an axis (B.1-B.6);
-// the 2-D DFT is (FFT Omega <1>) over the rows followed by the same over the columns.
-// Rows: a batched lifted 1-D plan (batch n1, length n2).  Columns: one pass of
-// n1-point DFTs along the stride-n2 axis -- the middle-pass tile of §4 with the view
-// [1][n1][n2], no twiddle, in place -- so n1 <= FMAX.
-static int make_plan_2d(int64_t n1, int64_t n2, int sign, moa_fft_plan_s **res) {
+// Multi-dimensional transform of a row-major n_0 x ... x n_{r-1} array:
+// App. B's Omega applies a 1-D operation to every sub-array along an axis (B.1-B.6,
+// P:1495-1548), so the r-D DFT is the 1-D FFT applied along each axis in turn.
+// Last axis: a batched lifted 1-D plan (batch = product of the other extents, any
+// length).  Every other axis a: ONE pass of n_a-point DFTs along the stride
+// B = n_{a+1}...n_{r-1} axis -- the middle-pass tile of §4 with the view
+// [A = n_0...n_{a-1}][n_a][B], T adjacent columns per tile, no twiddle, in place --
+// so n_a <= FMAX for a < r-1.
+static int make_plan_nd(int rank, const int64_t *shape, int sign, moa_fft_plan_s **res) {
     *res = nullptr;
-    if (!pow2(n1) || n1 < 2 || n1 > FMAX)
-        return fail(MOA_ERR_INVALID_N, "n1=%lld must be 2^t1 with 1 <= t1 <= %d (one column pass)", (long long)n1,
-                    FMAX_LOG);
-    if (!pow2(n2) || n2 < 2 || n1 * n2 > ((int64_t)1 << 32))
-        return fail(MOA_ERR_INVALID_N, "n2=%lld must be 2^t2, t2 >= 1, with n1*n2 <= 2^32", (long long)n2);
+    if (rank < 2 || rank > 3) return fail(MOA_ERR_INVALID_ARG, "rank %d must be 2 or 3", rank);
     if (sign != -1 && sign != 1) return fail(MOA_ERR_INVALID_SIGN, "sign=%d must be -1 or +1", sign);
+    int64_t total = 1;
+    for (int a = 0; a < rank; ++a) {
+        const int64_t na = shape[a];
+        if (!pow2(na) || na < 2 || (a < rank - 1 && na > FMAX))
+            return fail(MOA_ERR_INVALID_N, "n%d=%lld must be 2^t with 1 <= t%s", a + 1, (long long)na,
+                        a < rank - 1 ? " <= 13 (one pass along a non-last axis)" : "");
+        total *= na;
+        if (total > ((int64_t)1 << 32))
+            return fail(MOA_ERR_INVALID_N, "the array holds more than 2^32 elements");
+    }
     moa_fft_options o;
     memset(&o, 0, sizeof o);
     o.mode = MOA_MODE_LIFTED;
-    o.batch = n1;
+    o.batch = total / shape[rank - 1];
     moa_fft_plan_s *rows = nullptr;
-    int rc = make_plan(n2, 1, sign, &o, &rows);
+    int rc = make_plan(shape[rank - 1], 1, sign, &o, &rows);
     if (rc) return rc;
     moa_fft_plan_s *pl = new moa_fft_plan_s();
     pl->rows = rows;
-    pl->n1 = n1;
-    pl->n2 = n2;
-    pl->n = n1 * n2;
-    pl->M = pl->n;
-    pl->t = ilog2(pl->n);
+    pl->n1 = shape[0];
+    pl->n2 = total / shape[0];
+    pl->n = total;
+    pl->M = total;
+    pl->t = ilog2(total);
     pl->sign = sign;
     pl->device = rows->device;
-    pl->d = 1;
-    pl->lift[0] = n1;
-    PassPlan pp;
-    memset(&pp.d, 0, sizeof(PassDesc));
-    PassDesc &D = pp.d;
-    pp.logF = ilog2(n1);
-    pp.T = choose_T(pp.logF, n2);
-    D.nmask = (uint64_t)n1 - 1;
-    D.hbits = rows->hbits;
-    D.tbits = pp.logF;
-    D.tw_hi = rows->tw_hi;
-    D.tw_lo = rows->tw_lo;
-    D.tw_f = rows->tw_f;
-    D.pack_lp = -1;
-    D.conj_in = D.conj_out = sign > 0;   // conj(DFT_-1(conj y)) along the columns
-    D.U = n2 / pp.T;
-    D.V = 1;
-    D.lU = ilog2(D.U);
-    D.lV = 0;
-    D.in_u = pp.T;
-    D.in_t = 1;
-    D.in_f = n2;
-    D.in_tfast = D.out_tfast = pp.T > 1;
-    D.out_u = D.in_u;
-    D.out_t = D.in_t;
-    D.out_k = D.in_f;
-    pp.tiles = D.U;
-    if (!pass_supported(pp.logF, pp.T)) {
-        free_plan(pl);
-        return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
+    pl->d = rank - 1;
+    for (int a = rank - 2; a >= 0; --a) {   // execution order: the last-but-one axis first
+        int64_t A = 1, B = 1;
+        for (int l = 0; l < a; ++l) A *= shape[l];
+        for (int l = a + 1; l < rank; ++l) B *= shape[l];
+        const int64_t F = shape[a];
+        PassPlan pp;
+        memset(&pp.d, 0, sizeof(PassDesc));
+        PassDesc &D = pp.d;
+        pp.logF = ilog2(F);
+        pp.T = choose_T(pp.logF, B);
+        D.nmask = (uint64_t)F - 1;
+        D.hbits = rows->hbits;
+        D.tbits = pp.logF;
+        D.tw_hi = rows->tw_hi;
+        D.tw_lo = rows->tw_lo;
+        D.tw_f = rows->tw_f;
+        D.pack_lp = -1;
+        D.conj_in = D.conj_out = sign > 0;   // conj(DFT_-1(conj y)) along this axis
+        D.U = B / pp.T;
+        D.V = A;
+        D.lU = ilog2(D.U);
+        D.lV = ilog2(D.V);
+        D.in_u = pp.T;
+        D.in_v = F * B;
+        D.in_t = 1;
+        D.in_f = B;
+        D.in_tfast = D.out_tfast = pp.T > 1;
+        D.out_u = D.in_u;
+        D.out_v = D.in_v;
+        D.out_t = D.in_t;
+        D.out_k = D.in_f;
+        pp.tiles = D.U * D.V;
+        if (!pass_supported(pp.logF, pp.T)) {
+            free_plan(pl);
+            return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
+        }
+        pl->passes.push_back(pp);
+        if (a + 1 < 4) pl->lift[a + 1] = F;
     }
-    pl->passes.push_back(pp);
+    pl->lift[0] = shape[rank - 1];
     pl->stream = rows->stream;
     *res = pl;
     return MOA_OK;
@@ -945,12 +962,14 @@ static int p2p_phase(moa_fft_plan_s *pl, const double2 *in, double2 *out, int ph
 
 static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
     cudaStream_t s = pl->stream;
-    if (pl->rows) {   // 2-D: (FFT Omega <1>) over the rows, then the column pass in place
+    if (pl->rows) {   // r-D: (FFT Omega) along the last axis, then one pass per other axis, in place
         pl->rows->stream = s;
         pl->rows->profiling = pl->profiling;
         int rc = execute(pl->rows, in, out);
         if (rc) return rc;
-        return launch_pp(pl, pl->passes[0], 1, out, out);
+        for (size_t i = 0; i < pl->passes.size(); ++i)
+            if ((rc = launch_pp(pl, pl->passes[i], (int)i + 1, out, out)) != MOA_OK) return rc;
+        return MOA_OK;
     }
     if (pl->mode == MOA_MODE_LITERAL) {
         // Fig 2.1 literally: (1) x <- P_n x; (2)-(7) t radix-2 stages (Fig 3.9)
@@ -1058,11 +1077,20 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
 
 moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign) { return moa_fft_plan_ex(n, p, sign, nullptr); }
 
-moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign) {
+moa_fft_plan_t moa_fft_plan_nd(int rank, const int64_t *shape, int sign) {
     g_err.clear();
+    if (!shape) {
+        fail(MOA_ERR_INVALID_ARG, "NULL shape");
+        return nullptr;
+    }
     moa_fft_plan_s *pl = nullptr;
-    if (make_plan_2d(n1, n2, sign, &pl) != MOA_OK) return nullptr;
+    if (make_plan_nd(rank, shape, sign, &pl) != MOA_OK) return nullptr;
     return pl;
+}
+
+moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign) {
+    const int64_t shape[2] = {n1, n2};
+    return moa_fft_plan_nd(2, shape, sign);
 }
 
 int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
@@ -1299,11 +1327,13 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
     }
     o->workspace_bytes = pl->workspace_bytes;
     o->batch = pl->batch;
-    if (pl->rows) {   // 2-D: the row plan's passes, then the column pass
-        o->passes = pl->rows->d + 1;
-        for (int i = 0; i < 4; ++i) o->lift[i] = i < pl->rows->d ? pl->rows->lift[i] : (i == pl->rows->d ? pl->n1 : 0);
-        o->launches = pl->rows->d + 1;
-        o->hbm_bytes = 32 * pl->n * (pl->rows->d + 1);
+    if (pl->rows) {   // r-D: the row plan's passes, then one pass per other axis
+        const int k = (int)pl->passes.size();
+        o->passes = pl->rows->d + k;
+        for (int i = 0; i < 4; ++i) o->lift[i] = i < pl->rows->d ? pl->rows->lift[i] : 0;
+        for (int i = 0; i < k && pl->rows->d + i < 4; ++i) o->lift[pl->rows->d + i] = (int64_t)1 << pl->passes[i].logF;
+        o->launches = pl->rows->d + k;
+        o->hbm_bytes = 32 * pl->n * (pl->rows->d + k);
         o->workspace_bytes = pl->rows->workspace_bytes;
         o->batch = 1;
     }

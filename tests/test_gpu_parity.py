@@ -203,6 +203,18 @@ def test_2d_transform(n1, n2):
         assert oracle.rel_l2(got, ref) <= tol(t), (n1, n2, sign)
 
 
+@pytest.mark.parametrize("shape", [(2, 2, 2), (4, 8, 16), (64, 32, 128), (16, 64, 1024), (8192, 2, 8),
+                                   (2, 8192, 8), (4, 4, 1 << 16)])
+def test_3d_transform(shape):
+    """N3: 3-D DFT via Omega, against oracle.fftn (pinned by the r-D sum)."""
+    n = int(np.prod(shape))
+    x = moa_inputs.complex_signal(0x3D00 + n, n).reshape(shape)
+    t = n.bit_length() - 1
+    for sign in (-1, 1):
+        got = _run(moa.PlanND(shape, sign), x.reshape(-1)).reshape(shape)
+        assert oracle.rel_l2(got, oracle.fftn(x, sign, threads=8)) <= tol(t), (shape, sign)
+
+
 def test_2d_rejects_bad_shapes():
     with pytest.raises(moa.MoaError):
         moa.Plan2D(1 << 14, 4)

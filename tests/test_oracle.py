@@ -351,3 +351,17 @@ def test_fft2_library_special_case():
     x = moa_inputs.complex_signal(0x2D, 64 * 128).reshape(64, 128)
     assert oracle.rel_l2(oracle.fft2(x, -1), np.fft.fft2(x)) <= 1e-14
     assert oracle.rel_l2(oracle.fft2(x, +1), np.fft.ifft2(x) * x.size) <= 1e-14
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2), (2, 4, 8), (4, 2, 4), (8, 8)])
+def test_fftn_equals_bruteforce_sum(shape):
+    x = moa_inputs.complex_signal(0x3D + sum(shape), int(np.prod(shape))).reshape(shape)
+    for sign in (-1, 1):
+        assert oracle.rel_l2(oracle.fftn(x, sign), oracle.dftn(x, sign)) <= 1e-14
+
+
+def test_fftn_matches_fft2_and_numpy():
+    x = moa_inputs.complex_signal(0x3E, 16 * 32 * 8).reshape(16, 32, 8)
+    assert oracle.rel_l2(oracle.fftn(x), np.fft.fftn(x)) <= 1e-14
+    y = x.reshape(16, 256)
+    assert np.array_equal(oracle.fftn(y), oracle.fft2(y))
