@@ -209,10 +209,38 @@ def run_ours(args, rank: int, world: int):
     moa.gen_uniform(moa_inputs.seed_for(t), M, x, first=rank, stride=world)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream(device=dev)
-    xchg = moa.XCHG_P2P if (world > 1 and args.exchange == "p2p") else moa.XCHG_NCCL
-    plan = moa.Plan(n, world, -1, stream=stream, exchange=xchg)
-    if xchg == moa.XCHG_P2P:
-        plan.enable_p2p()
+    plan = None
+    if world > 1 and args.exchange in ("p2p", "auto"):
+        # the fused NVLink exchange, admitted only if every rank reproduces the NCCL
+        # path's result bit for bit (same arithmetic, only the transport differs)
+        ok = 1
+        try:
+            cand = moa.Plan(n, world, -1, stream=stream, exchange=moa.XCHG_P2P)
+            cand.enable_p2p()
+            ref_plan = moa.Plan(n, world, -1, stream=stream)
+            with torch.cuda.stream(stream):
+                a = cand.execute(x)
+                b = ref_plan.execute(x)
+            stream.synchronize()
+            ok = int(torch.equal(a, b))
+            ref_plan.destroy()
+            del a, b
+        except Exception as e:  # noqa: BLE001 - any failure falls back to NCCL
+            print(f"p2p exchange unavailable ({e}); using NCCL", file=sys.stderr)
+            ok, cand = 0, None
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            plan = cand
+        else:
+            if args.exchange == "p2p":
+                raise RuntimeError("--exchange p2p: the fused exchange failed its bitwise check")
+            if cand is not None:
+                cand.destroy()
+    exchange_used = "p2p" if plan is not None else "nccl"
+    if plan is None:
+        plan = moa.Plan(n, world, -1, stream=stream)
+    args.exchange = exchange_used
     info = plan.info()
     lib = moa.load()
 
@@ -353,9 +381,10 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
                     help="p > 1 global transpose: NCCL send/recv group, or the last pass storing into the "
-                         "peers' receive buffers over CUDA-IPC/NVLink (MOA_XCHG_P2P)")
+                         "peers' receive buffers over CUDA-IPC/NVLink (MOA_XCHG_P2P); auto = P2P when it "
+                         "reproduces the NCCL result bitwise on every rank, else NCCL")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
