@@ -608,7 +608,6 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-    if (d.stagger_ns && blockIdx.x < 4u * d.stagger_sms) __nanosleep((blockIdx.x / d.stagger_sms) * d.stagger_ns);
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     tile_fft<F, T>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
                    blockIdx.x);

@@ -60,9 +60,6 @@ struct PassDesc {
     // offset by bi * bstride elements in src and dst (bstride 0 = no batch)
     int ltiles;
     int64_t bstride;
-    // first-wave stagger (ns per resident-CTA slot): desynchronises the load/compute
-    // phases of the CTAs that share an SM (0 = off)
-    int stagger_ns, stagger_sms;
     // programmatic dependent launch: the kernel is launched before its predecessor on
     // the stream has finished; it signals its own dependents at once and waits for the
     // predecessor's grid (griddepcontrol.wait) before touching global data

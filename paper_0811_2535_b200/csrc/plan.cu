@@ -479,13 +479,6 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
             }
         }
         D.pdl = env_int("MOA_FFT_PDL", 1);   // measured: 2^24 275.5 -> 271.4 us, 2^16 15.3 -> 13.3 us
-        D.stagger_ns = env_int("MOA_FFT_STAGGER", 0);
-        if (D.stagger_ns) {
-            int dev = 0, sms = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            D.stagger_sms = sms;
-        }
         if (!pow2(D.U) || !pow2(D.V))
             return fail(MOA_ERR_INVALID_ARG, "internal: tile grid %lld x %lld not powers of two", (long long)D.U,
                         (long long)D.V);
