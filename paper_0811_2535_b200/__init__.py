@@ -17,7 +17,7 @@ import os
 
 from . import build as _build
 
-__all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
+__all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "scatter_cyclic", "gather_cyclic", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
            "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
@@ -387,6 +387,45 @@ def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
     if rc:
         _err(rc)
     return int(F.value), a, b, c
+
+
+def scatter_cyclic(x0, n: int, group=None, device=None):
+    """The paper's DISTRIBUTE_CENTRALIZED_TO_CYCLIC_PARTITIONED (Fig 5.8):
+    rank 0 holds the whole x0 (n elements); rank r receives xcyclic = x0[r::p] (psize
+    elements).  Layout plumbing outside the transform (torch.distributed scatter);
+    `device` is where the local slice lives (default: x0's device on rank 0, CPU
+    elsewhere unless given)."""
+    import torch
+    import torch.distributed as dist
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    psize = n // p
+    dev = device if device is not None else (x0.device if rank == 0 else torch.device("cpu"))
+    mine = torch.empty(psize, dtype=torch.complex128, device=dev)
+    chunks = None
+    if rank == 0:
+        chunks = [x0[r::p].contiguous().view(torch.float64).to(dev) for r in range(p)]
+    out = mine.view(torch.float64)
+    dist.scatter(out, chunks, src=0, group=group)
+    return mine
+
+
+def gather_cyclic(xcyclic, n: int, group=None):
+    """The paper's DISTRIBUTE_CYCLIC_PARTITIONED_TO_CENTRALIZED (Fig 5.8):
+    rank r holds X[r::p]; rank 0 returns the whole n-vector in natural order (x0(r:n-1:m)
+    = xcyclic of rank r), the other ranks return None."""
+    import torch
+    import torch.distributed as dist
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    psize = n // p
+    flat = xcyclic.contiguous().view(torch.float64)
+    parts = [torch.empty_like(flat) for _ in range(p)] if rank == 0 else None
+    dist.gather(flat, parts, dst=0, group=group)
+    if rank != 0:
+        return None
+    x0 = torch.empty(n, dtype=torch.complex128, device=xcyclic.device)
+    for r in range(p):
+        x0[r::p] = parts[r].view(torch.complex128)[:psize]
+    return x0
 
 
 def bcast_unique_id(group=None) -> bytes:

@@ -96,3 +96,39 @@ def test_bench_reference_arm_torchrun_two_ranks():
     assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
     assert rec["cpu_baseline"]["kind"] == "oracle"
     assert rec["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _layout_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import moa_inputs
+        import paper_0811_2535_b200 as moa
+        n = 1 << 10
+        x0 = torch.from_numpy(moa_inputs.signal_for(10)) if rank == 0 else None
+        mine = moa.scatter_cyclic(x0, n)
+        ok_scatter = np.array_equal(mine.numpy(), moa_inputs.signal_for(10)[rank::world])
+        back = moa.gather_cyclic(mine, n)
+        ok_gather = (rank != 0) or np.array_equal(back.numpy(), moa_inputs.signal_for(10))
+        q.put((rank, bool(ok_scatter and ok_gather)))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_centralized_cyclic_layouts_over_gloo(world):
+    """Fig 5.8's centralized<->cyclic redistributions (scatter_cyclic /
+    gather_cyclic): rank r gets x[r::p]; gathering the cyclic slices restores x."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] is True for r in range(world)), res
