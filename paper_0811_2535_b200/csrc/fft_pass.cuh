@@ -20,6 +20,10 @@
 #pragma once
 #include <stdlib.h>
 
+// points per thread (the largest in-register radix).  Measured: 8 points per thread
+// (1024 threads/SM at <= 64 registers) is 20-35 % slower than 16 on B200.
+#define MOA_RMAX 16
+
 #include "moa_internal.h"
 #include "tma.cuh"
 
@@ -183,13 +187,13 @@ __device__ __forceinline__ int smem_idx(int t, int f) {
 // radix of the last Stockham stage of an F-point transform (radix 16 first, remainder last)
 __host__ __device__ constexpr int lrs(int F) {
     int ns = 1;
-    while (F / ns > 16) ns *= 16;
+    while (F / ns > MOA_RMAX) ns *= MOA_RMAX;
     return F / ns;
 }
 
 template <int F, int T>
 struct PassShape {
-    static constexpr int R = F >= 16 ? 16 : F;   // points per thread
+    static constexpr int R = F >= MOA_RMAX ? MOA_RMAX : F;   // points per thread
     static constexpr int NT = T * F / R;         // threads per CTA
     static constexpr int PAD = T == 1 ? 0 : (T == 2 ? 4 : (T == 4 ? 2 : 1));
     // last-stage geometry (for the per-tile twiddle tables)
@@ -199,12 +203,10 @@ struct PassShape {
     static constexpr size_t TWA = (size_t)T * (LNB + 1) * sizeof(double2);   // A[t][j] = w^(al_t + be_t j)
     static constexpr size_t TWB = (size_t)T * (LRS + 1) * sizeof(double2);   // B[t][r] = w^(be_t NB r)
     static constexpr size_t SMEM = XCH + TWA + TWB;
-#ifndef MOA_MINB_2048
-#define MOA_MINB_2048 4
-#endif
-    // small tiles: 512 resident threads per SM (<= 128 registers each) whatever the CTA size
-    static constexpr int MINB = (T * F <= 2048) ? (NT >= 128 ? MOA_MINB_2048 : (512 / NT > 16 ? 16 : 512 / NT))
-                                                : ((T * F <= 4096) ? 2 : 1);
+    // resident threads per SM: 512 at 16 points per thread (<= 128 registers each),
+    // 1024 at 8 points per thread (<= 64 registers)
+    static constexpr int TGT = 512 * 16 / MOA_RMAX;
+    static constexpr int MINB = TGT / NT < 1 ? 1 : (TGT / NT > 16 ? 16 : TGT / NT);
 };
 
 // Where one tile reads and writes (a persistent kernel retargets these per tile).
@@ -392,7 +394,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     constexpr int R = SH::R;
     constexpr int NT = SH::NT;
     constexpr int REM = F / NS;
-    constexpr int RS = REM >= 16 ? 16 : REM;   // radix of this stage
+    constexpr int RS = REM >= MOA_RMAX ? MOA_RMAX : REM;   // radix of this stage
     constexpr int NB = F / RS;                 // butterflies per transform
     constexpr int M = R / RS;                  // butterflies per thread
     constexpr bool LAST = (NS * RS == F);
@@ -564,7 +566,7 @@ template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, in
 __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
                                            const double2 *inbuf, const Hook &hook) {
     constexpr int REM = F / NS;
-    constexpr int RS = REM >= 16 ? 16 : REM;
+    constexpr int RS = REM >= MOA_RMAX ? MOA_RMAX : REM;
     fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
     if constexpr (NS * RS < F) fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
 }
@@ -631,7 +633,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int F, int T>
 __device__ __forceinline__ void prefetch_tile(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b) {
     using SH = PassShape<F, T>;
-    constexpr int RS = F >= 16 ? 16 : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
+    constexpr int RS = F >= MOA_RMAX ? MOA_RMAX : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
     const int64_t u = b & (d.U - 1);
     const int64_t v = (b >> d.lU) & (d.V - 1);
     const int64_t w = b >> (d.lU + d.lV);

@@ -17,7 +17,7 @@ int pass_supported(int logF, int T) {
 
 int pass_threads(int logF, int T) {
     int F = 1 << logF;
-    int R = F >= 16 ? 16 : F;
+    int R = F >= MOA_RMAX ? MOA_RMAX : F;
     return T * F / R;
 }
 
