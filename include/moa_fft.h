@@ -122,8 +122,9 @@ moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign);
  * operation to every sub-array along an axis (B.1-B.6), so the 2-D DFT
  *   X[k1][k2] = sum_{j1,j2} x[j1][j2] exp(sign*2*pi*i*(j1*k1/n1 + j2*k2/n2))
  * is the lifted 1-D FFT over the rows followed by the same over the columns.
- *   n1 = 2^t1, 1 <= t1 <= 13 (the column transforms are one pass), n2 = 2^t2 with
- *   t2 >= 1 (the rows are a batched lifted 1-D plan), n1 * n2 <= 2^32.
+ *   n1 = 2^t1, 1 <= t1 <= 26 (the column transforms: one pass up to 2^13, else two
+ *   lifted passes), n2 = 2^t2 with t2 >= 1 (the rows: a batched lifted 1-D plan),
+ *   n1 * n2 <= 2^32.
  * x, X: n1 x n2 complex128, row-major (element (j1, j2) at j1*n2 + j2).  Execute
  * with moa_fft_execute; in == out allowed.  NULL on error (moa_fft_last_error).
  */
@@ -133,8 +134,10 @@ moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign);
  * r-dimensional transform, r = 2 or 3, of a row-major shape[0] x ... x shape[r-1]
  * complex128 array: X[k] = sum_j x[j] exp(sign*2*pi*i * sum_a j_a*k_a/shape[a]).
  * The last axis is any power of two (a batched lifted 1-D plan); every other axis is
- * 2^t with 1 <= t <= 13 (one pass of DFTs along that strided axis, in place), in the
- * order last-but-one axis first.  The product of the extents is <= 2^32.  Execute
+ * 2^t with 1 <= t <= 26: one pass of DFTs along that strided axis, in place, for
+ * t <= 13, else two lifted passes through a plan-owned work buffer (twiddle
+ * omega_N^(j2*k1) between them, transposed store); last-but-one axis first.  The
+ * product of the extents is <= 2^32.  Execute
  * with moa_fft_execute; in == out allowed.  NULL on error.  (moa_fft_plan_2d is the
  * rank-2 case.)
  */

@@ -90,6 +90,7 @@ struct PassPlan {
     int tma = 0;
     int tma_grid = 0;
     int pf_grid = 0;   // > 0: prefetching persistent kernel (fft_pass_pf_kernel)
+    int io = 0;        // r-D axis passes: 0 = out -> out (in place), 1 = out -> work, 2 = work -> out
     CUtensorMap map;
     const void *map_base = nullptr;
 };
@@ -204,6 +205,7 @@ struct moa_fft_plan_s {
     int hbits = 0;
     cudaStream_t stream = nullptr;
     double2 *tw_hi = nullptr, *tw_lo = nullptr, *tw_f = nullptr;
+    std::vector<double2 *> axis_tw;   // r-D plans: two-level omega_N tables of lifted non-last axes
     double2 *work = nullptr, *send = nullptr, *recv = nullptr;
     double2 *stage_in = nullptr, *stage_out = nullptr;  // execute_host staging
     // execute_host_batch: second staging pair + copy streams and events (lazily created)
@@ -503,6 +505,7 @@ static void free_plan(moa_fft_plan_s *pl) {
     cudaStreamSynchronize(pl->stream);
     for (int r = 0; r < 16; ++r)
         if (pl->peer_mapped[r]) cudaIpcCloseMemHandle(pl->peer_recv[r]);
+    for (double2 *p : pl->axis_tw) cudaFree(p);
     cudaFree(pl->tw_hi);
     cudaFree(pl->tw_lo);
     cudaFree(pl->tw_f);
@@ -784,9 +787,9 @@ static int make_plan_nd(int rank, const int64_t *shape, int sign, moa_fft_plan_s
     int64_t total = 1;
     for (int a = 0; a < rank; ++a) {
         const int64_t na = shape[a];
-        if (!pow2(na) || na < 2 || (a < rank - 1 && na > FMAX))
+        if (!pow2(na) || na < 2 || (a < rank - 1 && na > (int64_t)FMAX * FMAX))
             return fail(MOA_ERR_INVALID_N, "n%d=%lld must be 2^t with 1 <= t%s", a + 1, (long long)na,
-                        a < rank - 1 ? " <= 13 (one pass along a non-last axis)" : "");
+                        a < rank - 1 ? " <= 26 (at most two passes along a non-last axis)" : "");
         total *= na;
         if (total > ((int64_t)1 << 32))
             return fail(MOA_ERR_INVALID_N, "the array holds more than 2^32 elements");
@@ -808,44 +811,129 @@ static int make_plan_nd(int rank, const int64_t *shape, int sign, moa_fft_plan_s
     pl->sign = sign;
     pl->device = rows->device;
     pl->d = rank - 1;
-    for (int a = rank - 2; a >= 0; --a) {   // execution order: the last-but-one axis first
-        int64_t A = 1, B = 1;
-        for (int l = 0; l < a; ++l) A *= shape[l];
-        for (int l = a + 1; l < rank; ++l) B *= shape[l];
-        const int64_t F = shape[a];
+    auto axis_pass = [&](int logF, int64_t B) {
         PassPlan pp;
         memset(&pp.d, 0, sizeof(PassDesc));
+        pp.logF = logF;
+        pp.T = choose_T(logF, B);
         PassDesc &D = pp.d;
-        pp.logF = ilog2(F);
-        pp.T = choose_T(pp.logF, B);
-        D.nmask = (uint64_t)F - 1;
         D.hbits = rows->hbits;
-        D.tbits = pp.logF;
         D.tw_hi = rows->tw_hi;
         D.tw_lo = rows->tw_lo;
         D.tw_f = rows->tw_f;
         D.pack_lp = -1;
-        D.conj_in = D.conj_out = sign > 0;   // conj(DFT_-1(conj y)) along this axis
-        D.U = B / pp.T;
-        D.V = A;
-        D.lU = ilog2(D.U);
-        D.lV = ilog2(D.V);
-        D.in_u = pp.T;
-        D.in_v = F * B;
         D.in_t = 1;
-        D.in_f = B;
+        D.out_t = 1;
         D.in_tfast = D.out_tfast = pp.T > 1;
-        D.out_u = D.in_u;
-        D.out_v = D.in_v;
-        D.out_t = D.in_t;
-        D.out_k = D.in_f;
-        pp.tiles = D.U * D.V;
+        D.U = B / pp.T;
+        D.lU = ilog2(D.U);
+        D.in_u = D.out_u = pp.T;
+        return pp;
+    };
+    bool need_work = false;
+    for (int a = rank - 2; a >= 0; --a) {   // execution order: the last-but-one axis first
+        int64_t A = 1, B = 1;
+        for (int l = 0; l < a; ++l) A *= shape[l];
+        for (int l = a + 1; l < rank; ++l) B *= shape[l];
+        const int64_t N = shape[a];
+        if (N <= FMAX) {   // one pass, in place: view [A][N][B]
+            PassPlan pp = axis_pass(ilog2(N), B);
+            PassDesc &D = pp.d;
+            D.nmask = (uint64_t)N - 1;
+            D.tbits = pp.logF;
+            D.conj_in = D.conj_out = sign > 0;   // conj(DFT_-1(conj y)) along this axis
+            D.V = A;
+            D.lV = ilog2(D.V);
+            D.in_v = D.out_v = N * B;
+            D.in_f = D.out_k = B;
+            pp.tiles = D.U * D.V;
+            pl->passes.push_back(pp);
+        } else {
+            // a lifted strided axis, N = N1 * N2 (the reshape-transpose of §4 along axis a):
+            // element (alpha, j1, j2, beta) at ((alpha*N1 + j1)*N2 + j2)*B + beta.
+            //   pass A (out -> work): N1-point DFTs over j1 (stride N2*B), times omega_N^(j2*k1)
+            //   pass B (work -> out): N2-point DFTs over j2 (stride B), stored at
+            //                         (alpha*N + k1 + N1*k2)*B + beta (the transposed store)
+            const int tN = ilog2(N), t1 = tN / 2, t2 = tN - t1;
+            const int64_t N1 = (int64_t)1 << t1, N2 = (int64_t)1 << t2;
+            const int hb = (tN + 1) / 2;
+            const int64_t nlo = (int64_t)1 << hb, nhi = (int64_t)1 << (tN - hb);
+            std::vector<double2> hlo(nlo), hhi(nhi);
+            for (int64_t e = 0; e < nlo; ++e) hlo[e] = host_root((uint64_t)e, (uint64_t)N);
+            for (int64_t e = 0; e < nhi; ++e) hhi[e] = host_root((uint64_t)e << hb, (uint64_t)N);
+            double2 *dlo = nullptr, *dhi = nullptr;
+            if (cudaMalloc((void **)&dlo, nlo * 16) != cudaSuccess || cudaMalloc((void **)&dhi, nhi * 16) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(dlo);
+                free_plan(pl);
+                return fail(MOA_ERR_OOM, "axis twiddle tables");
+            }
+            pl->axis_tw.push_back(dlo);
+            pl->axis_tw.push_back(dhi);
+            if (cudaMemcpy(dlo, hlo.data(), nlo * 16, cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(dhi, hhi.data(), nhi * 16, cudaMemcpyHostToDevice) != cudaSuccess) {
+                free_plan(pl);
+                return fail(MOA_ERR_CUDA, "axis twiddle upload failed");
+            }
+            PassPlan pa = axis_pass(t1, B);
+            {
+                PassDesc &D = pa.d;
+                D.nmask = (uint64_t)N - 1;
+                D.tbits = tN;
+                D.hbits = hb;
+                D.tw_hi = dhi;
+                D.tw_lo = dlo;
+                D.conj_in = sign > 0;
+                D.twiddle = 1;
+                D.b_v = 1;   // exponent j2 * k1 (v = j2)
+                D.V = N2;
+                D.lV = t2;
+                D.in_v = D.out_v = B;
+                D.in_w = D.out_w = N * B;
+                D.in_f = D.out_k = N2 * B;
+                pa.tiles = D.U * D.V * A;
+                pa.io = 1;
+            }
+            PassPlan pb = axis_pass(t2, B);
+            {
+                PassDesc &D = pb.d;
+                D.nmask = (uint64_t)N - 1;
+                D.tbits = tN;
+                D.conj_out = sign > 0;
+                D.V = N1;
+                D.lV = t1;
+                D.in_v = N2 * B;
+                D.in_w = N * B;
+                D.in_f = B;
+                D.out_v = B;
+                D.out_w = N * B;
+                D.out_k = N1 * B;
+                pb.tiles = D.U * D.V * A;
+                pb.io = 2;
+            }
+            if (!pass_supported(pa.logF, pa.T) || !pass_supported(pb.logF, pb.T)) {
+                free_plan(pl);
+                return fail(MOA_ERR_INVALID_ARG, "no pass kernel for an axis of length 2^%d", tN);
+            }
+            pl->passes.push_back(pa);
+            pl->passes.push_back(pb);
+            need_work = true;
+        }
+        if (a + 1 < 4) pl->lift[a + 1] = N;
+    }
+    for (const PassPlan &pp : pl->passes)
         if (!pass_supported(pp.logF, pp.T)) {
             free_plan(pl);
             return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
         }
-        pl->passes.push_back(pp);
-        if (a + 1 < 4) pl->lift[a + 1] = F;
+    if (need_work) {
+        if (cudaMalloc((void **)&pl->work, (size_t)total * sizeof(double2)) != cudaSuccess) {
+            cudaGetLastError();
+            free_plan(pl);
+            return fail(MOA_ERR_OOM, "r-D work buffer (%lld elements)", (long long)total);
+        }
+        pl->work_elems = total;
+        pl->workspace_bytes += total * 16;
     }
     pl->lift[0] = shape[rank - 1];
     pl->stream = rows->stream;
@@ -960,8 +1048,12 @@ static int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
         pl->rows->profiling = pl->profiling;
         int rc = execute(pl->rows, in, out);
         if (rc) return rc;
-        for (size_t i = 0; i < pl->passes.size(); ++i)
-            if ((rc = launch_pp(pl, pl->passes[i], (int)i + 1, out, out)) != MOA_OK) return rc;
+        for (size_t i = 0; i < pl->passes.size(); ++i) {
+            PassPlan &pp = pl->passes[i];
+            const double2 *src = pp.io == 2 ? pl->work : out;
+            double2 *dst = pp.io == 1 ? pl->work : out;
+            if ((rc = launch_pp(pl, pp, (int)i + 1, src, dst)) != MOA_OK) return rc;
+        }
         return MOA_OK;
     }
     if (pl->mode == MOA_MODE_LITERAL) {

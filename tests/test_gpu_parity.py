@@ -215,9 +215,21 @@ def test_3d_transform(shape):
         assert oracle.rel_l2(got, oracle.fftn(x, sign, threads=8)) <= tol(t), (shape, sign)
 
 
+@pytest.mark.parametrize("shape", [(1 << 14, 64), (1 << 15, 8), (2, 1 << 14, 4), (1 << 14, 2, 16), (1 << 17, 2)])
+def test_nd_lifted_long_axes(shape):
+    """N3: a non-last axis longer than 2^13 runs as two lifted passes along the strided
+    axis (twiddle omega_N^(j2 k1), transposed store) -- against oracle.fftn."""
+    n = int(np.prod(shape))
+    x = moa_inputs.complex_signal(0x4D00 + n + len(shape), n).reshape(shape)
+    t = n.bit_length() - 1
+    for sign in (-1, 1):
+        got = _run(moa.PlanND(shape, sign), x.reshape(-1)).reshape(shape)
+        assert oracle.rel_l2(got, oracle.fftn(x, sign, threads=8)) <= tol(t), (shape, sign)
+
+
 def test_2d_rejects_bad_shapes():
     with pytest.raises(moa.MoaError):
-        moa.Plan2D(1 << 14, 4)
+        moa.Plan2D(1 << 27, 4)
     with pytest.raises(moa.MoaError):
         moa.Plan2D(12, 16)
 
