@@ -464,8 +464,9 @@ static int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<P
         }
         if (pl->batch > 1) {
             if (d == 1) {
-                // tiles of T whole transforms (rows of n elements), one tile per group of T
-                int T = choose_T(pp.logF, pl->batch & -pl->batch);
+                // tiles of T whole transforms (rows of n elements), one tile per group of T;
+                // measured (tools/batch_probe.py): one transform per CTA from F = 1024 on
+                int T = pp.logF >= 10 ? 1 : choose_T(pp.logF, pl->batch & -pl->batch);
                 pp.T = T;
                 D.in_t = pl->n;
                 D.out_t = pl->n;
