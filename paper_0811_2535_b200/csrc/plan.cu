@@ -271,7 +271,7 @@ static int default_lifting(int tl, int64_t *lift, int p) {
         lift[1] = (int64_t)1 << (tl - a);
         return 2;
     }
-    if (tl == 25 || tl == 26) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
+    if (tl >= 25 && tl <= 27) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
         lift[0] = 256;
         lift[1] = 256;
         lift[2] = (int64_t)1 << (tl - 16);
@@ -310,8 +310,8 @@ static int choose_T(int logF, int64_t avail) {
     // tile size cap: long transforms take T*F = 8192 (one 128 KiB tile per SM);
     // short ones 4096 (2-3 tiles per SM overlap memory and FP64 work)
     // measured on B200 (tools/perf_probe.py): 2048-element tiles (4 CTAs/SM) for F <= 256,
-    // 4096 for F = 512, 1024 (T = 8, 4: >= 64-byte column runs), one 8192 tile above
-    int tf_max = env_int("MOA_FFT_TF", logF >= 11 ? TF_MAX : (logF >= 9 ? 4096 : 2048));
+    // 4096 for F = 512 .. 2048 (T = 8, 4, 2), one 8192 tile above
+    int tf_max = env_int("MOA_FFT_TF", logF >= 12 ? TF_MAX : (logF >= 9 ? 4096 : 2048));
     if (tf_max > TF_MAX) tf_max = TF_MAX;
     int T = 1;
     while (T < 64 && ((int64_t)(2 * T) << logF) <= tf_max && 2 * T <= avail) T *= 2;
