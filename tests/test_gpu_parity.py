@@ -145,7 +145,7 @@ def test_plan_info():
     assert info["passes"] == 2 and info["hbm_bytes"] == 32 * (1 << 24) * 2
     assert info["breakpoint"] == 25
     info = moa.Plan(1 << 27).info()
-    assert info["passes"] == 3 and info["lift"] == [2048, 256, 256]
+    assert info["passes"] == 3 and info["lift"] == [256, 256, 2048]
     info = moa.Plan(1 << 28).info()   # four levels from 2^28 (DESIGN.md §4 lifting table)
     assert info["passes"] == 4 and info["lift"] == [64, 64, 256, 256]
 
