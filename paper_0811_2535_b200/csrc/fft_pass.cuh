@@ -104,49 +104,13 @@ __device__ __forceinline__ Tp *elem_off_c(Tp *p, uint32_t c, uint32_t stride) {
     return reinterpret_cast<Tp *>(reinterpret_cast<uintptr_t>(p) + (uint64_t)(16u * c) * (uint64_t)stride);
 }
 
-// omega_n^e from the two-level table: hi[e >> h] * lo[e & (2^h - 1)]
-__device__ __forceinline__ double2 tw2(const double2 *__restrict__ hi, const double2 *__restrict__ lo,
-                                       uint32_t e, int h) {
-    return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((1u << h) - 1))));
-}
 
-// q[r] = omega^(e0 + r*delta) for r < RS, from 1 + log2(RS) table lookups and
-// at most log2(RS) products per entry.
-template <int RS>
-__device__ __forceinline__ void twiddle_run(double2 *q, const PassDesc &d, uint32_t e0, uint32_t delta) {
-    const uint32_t nm = (uint32_t)d.nmask;
-    q[0] = tw2(d.tw_hi, d.tw_lo, e0 & nm, d.hbits);
-    if (RS == 1) return;
-    double2 p1 = tw2(d.tw_hi, d.tw_lo, delta & nm, d.hbits);
-    q[1] = cmul(q[0], p1);
-    if (RS == 2) return;
-    double2 p2 = tw2(d.tw_hi, d.tw_lo, (2 * delta) & nm, d.hbits);
-    q[2] = cmul(q[0], p2);
-    q[3] = cmul(q[1], p2);
-    if (RS == 4) return;
-    double2 p4 = tw2(d.tw_hi, d.tw_lo, (4 * delta) & nm, d.hbits);
-#pragma unroll
-    for (int r = 4; r < 8 && r < RS; ++r) q[r] = cmul(q[r - 4], p4);
-    if (RS == 8) return;
-    double2 p8 = tw2(d.tw_hi, d.tw_lo, (8 * delta) & nm, d.hbits);
-#pragma unroll
-    for (int r = 8; r < RS; ++r) q[r] = cmul(q[r - 8], p8);
-}
-
-// stage twiddles omega_{Ns*RS}^(r*k) = omega_FMAX^(r*e1), e1 = k*FMAX/(Ns*RS).
-//   MOA_STW_LOAD 1: one L1-resident table load per point (no products);
-//   MOA_STW_LOAD 0: 4 table loads (r = 1, 2, 4, 8) and products for the rest
-//                   (fewer loads on the latency-critical path between the stages)
-#ifndef MOA_STW_LOAD
-#define MOA_STW_LOAD 0
-#endif
+// stage twiddles omega_{Ns*RS}^(r*k) = omega_FMAX^(r*e1), e1 = k*FMAX/(Ns*RS): 4 table
+// loads (r = 1, 2, 4, 8) and products for the rest.  (One table load per point was
+// measured slower: more loads on the latency-critical path between the stages.)
 template <int RS>
 __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restrict__ tf, int e1) {
     if (RS == 1 || e1 == 0) return;
-#if MOA_STW_LOAD
-#pragma unroll
-    for (int r = 1; r < RS; ++r) x[r] = cmul(x[r], __ldg(tf + r * e1));
-#else
     double2 w1 = __ldg(tf + e1);
     double2 w2 = RS > 2 ? __ldg(tf + 2 * e1) : w1;
     double2 w4 = RS > 4 ? __ldg(tf + 4 * e1) : w1;
@@ -171,7 +135,6 @@ __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restr
     x[13] = cmul(x[13], cmul(w5, w8));
     x[14] = cmul(x[14], cmul(w6, w8));
     x[15] = cmul(x[15], cmul(w7, w8));
-#endif
 }
 
 // shared-memory address of element f of row t: rows padded so T-fastest lane
@@ -272,11 +235,6 @@ struct NoHook {
 // XOR-fold swizzle of a row-local point index (see smem_idx)
 __host__ __device__ constexpr int swz(int f) { return ((f >> 3) ^ (f >> 6) ^ (f >> 9) ^ (f >> 12)) & 7; }
 
-// flip the sign of the imaginary part when mask = 0x80000000 (conj without a select)
-__device__ __forceinline__ double2 conj_mask(double2 v, unsigned mask) {
-    v.y = __hiloint2double(__double2hiint(v.y) ^ (int)mask, __double2loint(v.y));
-    return v;
-}
 
 // Per-tile values shared by the stages of one tile.
 struct TileCtx {
@@ -296,12 +254,9 @@ __device__ __forceinline__ double2 root_pi(uint32_t e, int t) {
     return make_double2(c, s);
 }
 
-// Build the tile's twiddle tables: omega^(al_t + be_t*(j + r*NB)) = A[t][j] * B[t][r]
-//   MOA_PTW_SINCOS 1: sincospi of the exact rational exponent (FP64 work, no loads);
-//   MOA_PTW_SINCOS 0: the plan's two-level omega_n table (2 loads + 1 product)
-#ifndef MOA_PTW_SINCOS
-#define MOA_PTW_SINCOS 1
-#endif
+// Build the tile's twiddle tables: omega^(al_t + be_t*(j + r*NB)) = A[t][j] * B[t][r],
+// by sincospi of the exact rational exponent (FP64 work, no loads: the two-level table
+// lookup was measured slower, its loads sit on the tile's critical path)
 // (computed at tile start from the plan's two-level omega_n table -- one product per
 // entry; the stages' barriers publish them).
 template <int F, int T>
@@ -314,71 +269,14 @@ __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 
         if (i < T * NB) {
             const int t = i / NB, j = i % NB;
             const uint32_t a = al + (uint32_t)t * (uint32_t)d.a_t, b = be + (uint32_t)t * (uint32_t)d.b_t;
-#if MOA_PTW_SINCOS
             twa[t * (NB + 1) + j] = root_pi((a + b * (uint32_t)j) & nm, d.tbits);
-#else
-            twa[t * (NB + 1) + j] = tw2(d.tw_hi, d.tw_lo, (a + b * (uint32_t)j) & nm, d.hbits);
-#endif
         } else {
             const int k = i - T * NB, t = k / RS, r = k % RS;
             const uint32_t b = be + (uint32_t)t * (uint32_t)d.b_t;
-#if MOA_PTW_SINCOS
             twb[t * (RS + 1) + r] = root_pi((b * (uint32_t)(NB * r)) & nm, d.tbits);
-#else
-            twb[t * (RS + 1) + r] = tw2(d.tw_hi, d.tw_lo, (b * (uint32_t)(NB * r)) & nm, d.hbits);
-#endif
         }
     }
 }
-
-// Early-issued pass-twiddle operands (MOA_PTW_EARLY): the two-level table loads of the
-// (at most EPT) entries this thread builds are issued BEFORE the tile's input loads, so
-// they return (L2 hits) while the inputs are still in flight; the products and stores
-// into the tile tables happen after the input gather.
-#ifndef MOA_PTW_EARLY
-#define MOA_PTW_EARLY 0
-#endif
-#ifndef MOA_CONJ_LOP
-#define MOA_CONJ_LOP 0
-#endif
-template <int F, int T>
-struct TwEarly {
-    using SH = PassShape<F, T>;
-    static constexpr int ENT = T * (SH::LNB + SH::LRS);
-    static constexpr int EPT = (ENT + SH::NT - 1) / SH::NT;
-    double2 hi[EPT], lo[EPT];
-    __device__ __forceinline__ void issue(const PassDesc &d, uint32_t al, uint32_t be) {
-        constexpr int NB = SH::LNB, RS = SH::LRS;
-        const uint32_t nm = (uint32_t)d.nmask;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int i = threadIdx.x + q * SH::NT;
-            uint32_t e = 0;
-            if (i < T * NB) {
-                const int t = i / NB, j = i % NB;
-                e = (al + (uint32_t)t * (uint32_t)d.a_t + (be + (uint32_t)t * (uint32_t)d.b_t) * (uint32_t)j) & nm;
-            } else if (i < ENT) {
-                const int k = i - T * NB, t = k / RS, r = k % RS;
-                e = ((be + (uint32_t)t * (uint32_t)d.b_t) * (uint32_t)(NB * r)) & nm;
-            }
-            hi[q] = __ldg(d.tw_hi + (e >> d.hbits));
-            lo[q] = __ldg(d.tw_lo + (e & ((1u << d.hbits) - 1)));
-        }
-    }
-    __device__ __forceinline__ void finish(double2 *twa, double2 *twb) const {
-        constexpr int NB = SH::LNB, RS = SH::LRS;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int i = threadIdx.x + q * SH::NT;
-            if (i < T * NB) {
-                twa[(i / NB) * (NB + 1) + i % NB] = cmul(hi[q], lo[q]);
-            } else if (i < ENT) {
-                const int k = i - T * NB;
-                twb[(k / RS) * (RS + 1) + k % RS] = cmul(hi[q], lo[q]);
-            }
-        }
-    }
-};
 
 // One Stockham stage: Ns = product of the radices already applied.
 //   SRC 0: the first stage gathers from global memory; SRC 1/2: from the TMA
@@ -423,10 +321,6 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     // ---- gather inputs (the first stage then builds the tile's twiddle tables while
     //      its loads are in flight)
     if constexpr (FIRST && SRC == 0) {
-#if MOA_PTW_EARLY
-        TwEarly<F, T> twe;
-        if (d.twiddle) twe.issue(d, c.al, c.be);
-#endif
         // element offsets inside the tile's span fit 32 bits (span < n <= 2^32)
         const uint32_t sf = (uint32_t)NB * (uint32_t)d.in_f;
 #pragma unroll
@@ -435,23 +329,11 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int r = 0; r < RS; ++r) x[i * RS + r] = ld_io<LD>(elem_off_c(p, r, sf), pol);
         }
-#if MOA_CONJ_LOP
-        {   // sign flip of the imaginary parts on the integer pipe (mask 0 for sign -1)
-            const unsigned cm = d.conj_in ? 0x80000000u : 0u;
-#pragma unroll
-            for (int k = 0; k < R; ++k) x[k] = conj_mask(x[k], cm);
-        }
-#else
         if (d.conj_in) {
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
-#endif
-#if MOA_PTW_EARLY
-        if (d.twiddle) twe.finish(const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb));
-#else
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
-#endif
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
     } else if constexpr (FIRST && SRC == 3) {
         // prefetched by this same thread (cp.async, fft_pass_pf_kernel) into the
@@ -532,18 +414,10 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
                 for (int r = 1; r < RS; ++r) v[r] = cmul(v[r], cmul(a, c.twb[t * (RS + 1) + r]));
             }
-#if MOA_CONJ_LOP
-            {
-                const unsigned cm = d.conj_out ? 0x80000000u : 0u;
-#pragma unroll
-                for (int r = 0; r < RS; ++r) v[r] = conj_mask(v[r], cm);
-            }
-#else
             if (d.conj_out) {
 #pragma unroll
                 for (int r = 0; r < RS; ++r) v[r].y = -v[r].y;
             }
-#endif
             if (d.pack_lp >= 0) {   // general pack (single-level local transform, p > 1)
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {

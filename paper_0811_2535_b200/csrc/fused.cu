@@ -20,10 +20,6 @@
 // whatever the residency.  Counters are monotone across executes (epoch).
 #include "fft_pass.cuh"
 
-#ifndef MOA_FUSE_ACQ
-#define MOA_FUSE_ACQ 1
-#endif
-
 namespace moa {
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
@@ -53,9 +49,9 @@ __device__ __forceinline__ void wait_geq(const unsigned long long *p, unsigned l
     }
 }
 
-// Ticket-kernel wait: poll relaxed (an acquire load compiles to an L1 invalidation,
-// CCTL.IVALL, which would evict the twiddle tables of every CTA on the SM), then one
-// acquire once the target is reached.  The consumer reads the producer's data with
+// Ticket-kernel wait: poll relaxed, then one acquire once the target is reached (an
+// acquire load compiles to an L1 invalidation, CCTL.IVALL; polling with it would
+// invalidate L1 on every spin).  The consumer reads the producer's data with
 // ld.global.cg (L2) only.
 __device__ __forceinline__ void wait_geq_relaxed(const unsigned long long *p, unsigned long long target) {
     if (ld_relaxed_u64(p) < target) {
@@ -65,9 +61,7 @@ __device__ __forceinline__ void wait_geq_relaxed(const unsigned long long *p, un
             if (ns < 512) ns <<= 1;
         }
     }
-#if MOA_FUSE_ACQ
     (void)ld_acquire_u64(p);
-#endif
 }
 
 template <int F2, int T2, int F3, int T3>
