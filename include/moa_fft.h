@@ -258,6 +258,14 @@ int moa_fft_enable_p2p(moa_fft_plan_t plan);
  */
 int moa_fft_execute_phase(moa_fft_plan_t plan, const void *in, void *out, int phase);
 
+/*
+ * Host-only (no GPU needed): the default lifting <F1..Fd> the plan builder chooses
+ * for an n-point transform over p ranks (of the local length n/p).  lift_out has
+ * room for 4 factors; *d_out receives d.  Returns MOA_OK or MOA_ERR_INVALID_N /
+ * MOA_ERR_INVALID_P (same bounds as moa_fft_plan) / MOA_ERR_INVALID_ARG (NULL).
+ */
+int moa_fft_default_lifting(int64_t n, int p, int64_t *lift_out, int *d_out);
+
 /* Thread-local description of the last error ("" if none). */
 const char *moa_fft_last_error(void);
 

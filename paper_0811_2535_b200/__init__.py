@@ -57,7 +57,7 @@ EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execut
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
            "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase",
-           "moa_fft_plan_2d", "moa_fft_plan_nd"]
+           "moa_fft_plan_2d", "moa_fft_plan_nd", "moa_fft_default_lifting"]
 
 _lib = None
 
@@ -85,6 +85,7 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_plan_2d.restype = vp
     lib.moa_fft_plan_nd.argtypes = [ci, vp, ci]
     lib.moa_fft_plan_nd.restype = vp
+    lib.moa_fft_default_lifting.argtypes = [i64, ci, vp, ctypes.POINTER(ci)]
     lib.moa_fft_execute.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host.argtypes = [vp, vp, vp]
     lib.moa_fft_execute_host_batch.argtypes = [vp, ci, vp, vp]
@@ -426,6 +427,17 @@ def gather_cyclic(xcyclic, n: int, group=None):
     for r in range(p):
         x0[r::p] = parts[r].view(torch.complex128)[:psize]
     return x0
+
+
+def default_lifting(n: int, p: int = 1) -> list:
+    """The plan builder's default lifting <F1..Fd> of n/p (host only, no GPU)."""
+    lib = load()
+    lift = (ctypes.c_int64 * 4)()
+    d = ctypes.c_int(0)
+    rc = lib.moa_fft_default_lifting(int(n), int(p), lift, ctypes.byref(d))
+    if rc:
+        _err(rc)
+    return [int(lift[i]) for i in range(d.value)]
 
 
 def bcast_unique_id(group=None) -> bytes:

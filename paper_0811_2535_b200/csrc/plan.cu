@@ -1483,6 +1483,20 @@ int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opt
     return MOA_OK;
 }
 
+int moa_fft_default_lifting(int64_t n, int p, int64_t *lift_out, int *d_out) {
+    if (!lift_out || !d_out) return fail(MOA_ERR_INVALID_ARG, "NULL output");
+    if (!pow2(n) || n < 2 || n > ((int64_t)1 << 32))
+        return fail(MOA_ERR_INVALID_N, "n=%lld must be 2^t with 1 <= t <= 32", (long long)n);
+    if (!pow2(p) || p > 16 || n / p < p)
+        return fail(MOA_ERR_INVALID_P, "p=%d invalid for n=%lld (power of two, psize >= m, P:289)", p,
+                    (long long)n);
+    int64_t lift[4] = {0, 0, 0, 0};
+    const int d = default_lifting(ilog2(n / p), lift, p);
+    for (int i = 0; i < 4; ++i) lift_out[i] = lift[i];
+    *d_out = d;
+    return MOA_OK;
+}
+
 int moa_fft_set_profiling(moa_fft_plan_t pl, int enable) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
     pl->profiling = enable != 0;

@@ -92,3 +92,31 @@ def test_describe_pass_validation():
         moa.describe_pass(1 << 10, 1, 0, 5)
     with pytest.raises(moa.MoaError):
         moa.describe_pass(1 << 10, 4, 4, 0)
+
+
+def test_default_lifting_table_every_t_and_p():
+    """SURVEY §4.2 'lifting table for every t and P': the default lifting of n/p is a
+    factorisation into powers of two in [2, 2^13], at most 4 levels (3 when p > 1, the
+    pack layout's tile dimensions), first factor >= p for multi-level p > 1 plans, and
+    the documented table entries."""
+    for t in range(1, 33):
+        for p in (1, 2, 4, 8):
+            n = 1 << t
+            if n // p < p:
+                with pytest.raises(moa.MoaError):
+                    moa.default_lifting(n, p)
+                continue
+            lift = moa.default_lifting(n, p)
+            prod = 1
+            for f in lift:
+                assert f >= 2 and f <= 8192 and f & (f - 1) == 0, (t, p, lift)
+                prod *= f
+            assert prod == n // p, (t, p, lift)
+            assert len(lift) <= (3 if p > 1 else 4), (t, p, lift)
+            if p > 1 and len(lift) > 1:
+                assert lift[0] >= p, (t, p, lift)
+    assert moa.default_lifting(1 << 24) == [256, 256, 256]
+    assert moa.default_lifting(1 << 20) == [1024, 1024]
+    assert moa.default_lifting(1 << 26) == [256, 256, 1024]
+    assert moa.default_lifting(1 << 30) == [128, 128, 256, 256]
+    assert moa.default_lifting(1 << 10) == [1024]
