@@ -201,25 +201,11 @@ __device__ __forceinline__ void st_hint(double2 *p, double2 v, unsigned long lon
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
                  : "memory");
 }
-// streamed tile data: read-only path without an L1 allocation (MOA_LD_NOALLOC), so the
-// tile stream does not evict the L1-resident stage-twiddle table lines
-#ifndef MOA_LD_NOALLOC
-#define MOA_LD_NOALLOC 0
-#endif
-__device__ __forceinline__ double2 ld_noalloc(const double2 *p) {
-    double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
 template <int LD>
 __device__ __forceinline__ double2 ld_io(const double2 *p, unsigned long long pol) {
     if constexpr (LD == 1) return __ldcg(p);
     else if constexpr (LD == 2) return ld_hint(p, pol);
-#if MOA_LD_NOALLOC
-    else return ld_noalloc(p);
-#else
     else return __ldg(p);
-#endif
 }
 template <int ST>
 __device__ __forceinline__ void st_io(double2 *p, double2 v, unsigned long long pol) {
