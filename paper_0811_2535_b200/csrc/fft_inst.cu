@@ -51,6 +51,8 @@ cudaError_t MOA_CAT(launch_pass_tma_f, MOA_INST_LOGF)(int T, int src, const Pass
         if constexpr (tma_ok<TT, 1>()) {                                                   \
             if (src == 1) return launch_one_tma<kF, TT, 1>(d, map, tiles, grid, s);        \
             if (src == 2) return launch_one_tma<kF, TT, 2>(d, map, tiles, grid, s);        \
+            if (src == 4) return launch_one_tpf<kF, TT, 4>(d, map, tiles, grid, s);        \
+            if (src == 5) return launch_one_tpf<kF, TT, 5>(d, map, tiles, grid, s);        \
         }                                                                                  \
         return cudaErrorInvalidValue;                                                      \
     }
@@ -71,6 +73,8 @@ int MOA_CAT(grid_pass_tma_f, MOA_INST_LOGF)(int T, int src) {
         if constexpr (tma_ok<TT, 1>()) {                                \
             if (src == 1) return grid_one_tma<kF, TT, 1>();             \
             if (src == 2) return grid_one_tma<kF, TT, 2>();             \
+            if (src == 4) return grid_one_tpf<kF, TT, 4>();             \
+            if (src == 5) return grid_one_tpf<kF, TT, 5>();             \
         }                                                               \
         return 0;                                                       \
     }

@@ -298,6 +298,9 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     constexpr bool LAST = (NS * RS == F);
     constexpr int ROW = F + SH::PAD;           // shared row pitch
     const int tid = threadIdx.x;
+    // staging layout of a TMA-loaded tile: SRC 4/5 (single buffer, prefetch after the
+    // last stage's reads) stage like SRC 1/2 (column / row tiles)
+    constexpr int SL = SRC == 4 ? 1 : (SRC == 5 ? 2 : SRC);
 
     unsigned long long pol = 0;
     if constexpr (FIRST && LD == 2) pol = policy_evict_first();
@@ -306,9 +309,9 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         int b = tid + NT * i;
-        bool tfast = FIRST ? (SRC == 1 ? true : (SRC == 2 ? false : (bool)d.in_tfast))
+        bool tfast = FIRST ? (SL == 1 ? true : (SL == 2 ? false : (bool)d.in_tfast))
                            : (LAST ? (bool)d.out_tfast : false);
-        if (FIRST && LAST) tfast = SRC == 1 ? true : (SRC == 2 ? false : (bool)d.in_tfast);
+        if (FIRST && LAST) tfast = SL == 1 ? true : (SL == 2 ? false : (bool)d.in_tfast);
         if (T == 1) tfast = false;
         if (tfast) {
             tt[i] = b % T;
@@ -351,13 +354,13 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
         for (int i = 0; i < M; ++i)
 #pragma unroll
-            for (int r = 0; r < RS; ++r) x[i * RS + r] = inbuf[stage_idx<F, T, SRC>(tt[i], jj[i] + r * NB)];
+            for (int r = 0; r < RS; ++r) x[i * RS + r] = inbuf[stage_idx<F, T, SL>(tt[i], jj[i] + r * NB)];
         if (d.conj_in) {
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
-        hook();
+        if constexpr (SRC <= 2) hook();
     } else {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -373,7 +376,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         }
         // the exchange buffer is free once every lane has read it: the prefetching
         // kernel starts the next tile's copy into it here (hook = barrier + cp.async)
-        if constexpr (LAST && SRC == 3) hook();
+        if constexpr (LAST && SRC >= 3) hook();
     }
     // ---- twiddle + radix-RS butterflies in registers
 #pragma unroll
@@ -382,7 +385,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         dft_reg<RS>(x + i * RS);
     }
     if constexpr (!LAST) {
-        if (!FIRST || SRC == 3) __syncthreads();   // every lane has read before anyone overwrites
+        if (!FIRST || SRC >= 3) __syncthreads();   // every lane has read before anyone overwrites
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const int j = jj[i];
@@ -712,6 +715,87 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, (T * F <= 2048) ? MOA_TMA
         mbar_wait(&bar[b], (it >> 1) & 1);
         tile_fft<F, T, SRC, SyncHook>(buf(b), tw, d, io, tile, buf(b), SyncHook());
     }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent TMA pass with ONE staging buffer per CTA (SRC 4 = column tile, 5 = row
+// tile): the tile arrives by cp.async.bulk.tensor into the buffer that later holds the
+// shared-memory exchange; as soon as the last butterfly stage has read the exchange,
+// one elected thread starts the bulk copy of the CTA's next tile into the same buffer,
+// so that copy overlaps the last butterflies, the twiddles and the stores.  Same
+// shared memory as fft_pass_kernel (4 CTAs/SM at F*T = 2048); no per-thread copy
+// instructions (the cp.async variant flooded the MIO queue).
+template <int F, int T, int SRC>
+struct TpfShape {
+    static constexpr int SLAY = SRC == 4 ? 1 : 2;
+    using TS = TmaShape<F, T, SLAY>;
+    static constexpr size_t BUF = ((TS::IN_BYTES > PassShape<F, T>::XCH ? TS::IN_BYTES : PassShape<F, T>::XCH) + 127) / 128 * 128;
+    static constexpr size_t TW = PassShape<F, T>::TWA + PassShape<F, T>::TWB;
+    static constexpr size_t SMEM = 128 + BUF + TW + 16;
+};
+
+template <int F, int T, int SRC>
+struct TpfHook {
+    const CUtensorMap *map;
+    uint64_t *bar;
+    double2 *buf;
+    const PassDesc *d;
+    int64_t next, tiles;
+    __device__ __forceinline__ void operator()() const {
+        __syncthreads();   // every lane has read the exchange buffer
+        if (threadIdx.x == 0 && next < tiles) {
+            fence_proxy_async();   // the generic-proxy reads are ordered before the async writes
+            tma_issue_tile<F, T, TpfShape<F, T, SRC>::SLAY>(map, bar, buf, *d, next);
+        }
+    }
+};
+
+template <int F, int T, int SRC>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_tpf_kernel(const PassDesc d, const __grid_constant__ CUtensorMap tmap, int64_t tiles) {
+    using SH = TpfShape<F, T, SRC>;
+    extern __shared__ unsigned char smraw[];
+    unsigned char *base = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
+    double2 *buf = reinterpret_cast<double2 *>(base);
+    double2 *tw = reinterpret_cast<double2 *>(base + SH::BUF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + SH::BUF + SH::TW);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    int64_t tile = blockIdx.x;
+    if (tile >= tiles) return;
+    if (threadIdx.x == 0) tma_issue_tile<F, T, SH::SLAY>(&tmap, bar, buf, d, tile);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
+        mbar_wait(bar, it & 1);
+        const TpfHook<F, T, SRC> hk{&tmap, bar, buf, &d, tile + (int64_t)gridDim.x, tiles};
+        tile_fft<F, T, SRC, TpfHook<F, T, SRC>>(buf, tw, d, io, tile, buf, hk);
+        __syncthreads();   // the epilogue is done with the twiddle tables
+    }
+}
+
+template <int F, int T, int SRC>
+cudaError_t launch_one_tpf(const PassDesc &d, const CUtensorMap &map, int64_t tiles, int grid, cudaStream_t s) {
+    fft_pass_tpf_kernel<F, T, SRC><<<grid, PassShape<F, T>::NT, TpfShape<F, T, SRC>::SMEM, s>>>(d, map, tiles);
+    return cudaGetLastError();
+}
+
+template <int F, int T, int SRC>
+int grid_one_tpf() {
+    using SH = TpfShape<F, T, SRC>;
+    if (SH::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(fft_pass_tpf_kernel<F, T, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SH::SMEM) != cudaSuccess)
+        return 0;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft_pass_tpf_kernel<F, T, SRC>, PassShape<F, T>::NT,
+                                                      SH::SMEM) != cudaSuccess)
+        return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
 }
 
 template <int F, int T, int SRC>

@@ -121,7 +121,7 @@ static int encode_pass_map(PassPlan &pp, const void *base) {
     cuuint64_t dims[4], strides[3];
     cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
     cuuint32_t rank;
-    if (pp.tma == 1) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
+    if (pp.tma == 1 || pp.tma == 4) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
         const uint64_t B = (uint64_t)D.in_f, A = (uint64_t)D.V;
         rank = 3;
         dims[0] = 2 * B;
@@ -166,16 +166,18 @@ static void choose_tma(PassPlan &pp) {
         int g = pass_pf_grid(pp.logF, pp.T);
         if (g > 0) pp.pf_grid = (int)(g < pp.tiles ? g : pp.tiles);
     }
-    const char *tma_env = getenv("MOA_FFT_TMA");   // measured: the plain kernel (4 CTAs/SM) wins today
+    const char *tma_env = getenv("MOA_FFT_TMA");   // 1: double-buffered TMA, 2: single buffer + prefetch
     if (!tma_env || atoi(tma_env) == 0) return;
+    const int tma_kind = atoi(tma_env);
     const PassDesc &D = pp.d;
     int src = 0;
     if (!D.last && D.in_t == 1 && pp.T >= 2) src = 1;
     else if (D.last && D.in_f == 1) src = 2;
     if (!src) return;
-    int g = pass_tma_grid(pp.logF, pp.T, src);
+    const int code = tma_kind == 2 ? src + 3 : src;
+    int g = pass_tma_grid(pp.logF, pp.T, code);
     if (g <= 0) return;
-    pp.tma = src;
+    pp.tma = code;
     pp.tma_grid = g;
 }
 
