@@ -259,9 +259,10 @@ static int env_int(const char *name, int dflt) {
 }
 
 // default lifting <F1..Fd> of a local length 2^tl, from the B200 lifting sweeps
-// (tools/perf_probe.py): 256-point row passes (4 tiles per SM) wherever
-// the length allows, a single first factor up to 2^11, four levels from 2^28 on
-// (two <= 128-point column passes instead of one long one).  p > 1 plans keep <= 3 levels.
+// (tools/perf_probe.py): 256-point passes (4 tiles per SM) wherever the
+// length allows, the remaining factor in the row pass up to 2^12, four levels from 2^29
+// on (two <= 128-point column passes instead of one long one).  p > 1 plans keep <= 3
+// levels.
 static int default_lifting(int tl, int64_t *lift, int p) {
     if (tl <= FMAX_LOG) {
         lift[0] = (int64_t)1 << tl;
@@ -273,7 +274,7 @@ static int default_lifting(int tl, int64_t *lift, int p) {
         lift[1] = (int64_t)1 << (tl - a);
         return 2;
     }
-    if (tl >= 25 && tl <= 27) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
+    if (tl >= 25 && tl <= 28) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
         lift[0] = 256;
         lift[1] = 256;
         lift[2] = (int64_t)1 << (tl - 16);

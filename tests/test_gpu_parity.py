@@ -146,8 +146,10 @@ def test_plan_info():
     assert info["breakpoint"] == 25
     info = moa.Plan(1 << 27).info()
     assert info["passes"] == 3 and info["lift"] == [256, 256, 2048]
-    info = moa.Plan(1 << 28).info()   # four levels from 2^28 (DESIGN.md §4 lifting table)
-    assert info["passes"] == 4 and info["lift"] == [64, 64, 256, 256]
+    info = moa.Plan(1 << 28).info()
+    assert info["passes"] == 3 and info["lift"] == [256, 256, 4096]
+    info = moa.Plan(1 << 29).info()   # four levels from 2^29 (DESIGN.md §4 lifting table)
+    assert info["passes"] == 4 and info["lift"] == [64, 128, 256, 256]
 
 
 @pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_PF": "1"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "2"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
