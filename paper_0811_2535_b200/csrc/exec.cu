@@ -1,0 +1,218 @@
+// exec.cu -- the executor: per-kernel event profiling, pass launches, the p > 1
+// exchange phases and the execute() that strings them together (SURVEY §8(a)
+// S3-S9).  The plan objects come from plan.cu; the C ABI is abi.cu.
+#include <stdio.h>
+#include <string.h>
+
+#include "plan_internal.h"
+
+namespace moa {
+
+bool aligned16(const void *ptr) { return ptr && ((uintptr_t)ptr & 15) == 0; }
+
+// ---- event profiling: a scope records an event pair around one launch
+cudaEvent_t pool_event(moa_fft_plan_s *pl) {
+    if (!pl->pool.empty()) {
+        cudaEvent_t e = pl->pool.back();
+        pl->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    moa_fft_plan_s *pl;
+    int slot = -1;
+    cudaEvent_t a = nullptr;
+    ProfScope(moa_fft_plan_s *p, const std::string &name, int64_t bytes) : pl(p) {
+        if (!pl->profiling) return;
+        for (size_t i = 0; i < pl->slots.size(); ++i)
+            if (pl->slots[i].name == name) slot = (int)i;
+        if (slot < 0) {
+            pl->slots.push_back({name, bytes, 0, 0.0});
+            slot = (int)pl->slots.size() - 1;
+        }
+        a = pool_event(pl);
+        cudaEventRecord(a, pl->stream);
+    }
+    ~ProfScope() {
+        if (!pl->profiling || !a) return;
+        cudaEvent_t b = pool_event(pl);
+        cudaEventRecord(b, pl->stream);
+        pl->recs.push_back({slot, a, b});
+    }
+};
+
+// launch one pass (plain or TMA-staged) from src to dst; peers != NULL: the fused
+// exchange stores into peers[dst rank] + peer_off instead of dst
+int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, double2 *dst,
+              double2 *const *peers, int64_t peer_off) {
+    PassDesc D = pp.d;
+    D.src = src;
+    D.dst = dst;
+    if (peers) {
+        for (int r = 0; r < pl->p; ++r) D.peer[r] = peers[r];
+        D.peer_off = peer_off;
+    }
+    char name[64];
+    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : ""),
+             1 << pp.logF, pp.T,
+             peers ? "+push" : "");
+    ProfScope ps_(pl, name, 32 * pl->M * pl->batch);
+    cudaError_t e;
+    if (pp.tma && !peers) {
+        if (pp.map_base != (const void *)src) {
+            int rc = encode_pass_map(pp, src);
+            if (rc) return rc;
+        }
+        e = launch_pass_tma(pp.logF, pp.T, pp.tma, D, pp.map, pp.tiles, pp.tma_grid, pl->stream);
+    } else if (pp.pf_grid > 0) {
+        e = launch_pass_pf(pp.logF, pp.T, D, pp.tiles, pp.pf_grid, pl->stream);
+    } else {
+        e = launch_pass(pp.logF, pp.T, D, pp.tiles, pl->stream);
+    }
+    if (e != cudaSuccess)
+        return fail(MOA_ERR_CUDA, "pass %d (F=2^%d, T=%d, tma=%d) launch failed: %s", idx, pp.logF, pp.T, pp.tma,
+                    cudaGetErrorString(e));
+    return MOA_OK;
+}
+
+// run the lifted passes of one (virtual) rank: in -> [work] -> out (or -> peers)
+int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in, double2 *out,
+               double2 *const *peers, int64_t peer_off) {
+    const int d = (int)ps.size();
+    for (int i = 0; i < d; ++i) {
+        const bool last = i == d - 1;
+        int rc = launch_pp(pl, ps[i], i, (i == 0) ? in : pl->work, last ? out : pl->work, last ? peers : nullptr,
+                           peer_off);
+        if (rc) return rc;
+    }
+    return MOA_OK;
+}
+
+// P2P phase 1 (S5 + S6 + fused S7) / phase 2 (S8) on a real rank
+int p2p_phase(moa_fft_plan_s *pl, const double2 *in, double2 *out, int phase) {
+    const int P = pl->p;
+    const int64_t M = pl->M, chunk = M / P;
+    const int64_t half = (int64_t)(pl->xbuf & 1) * M;
+    if (phase == 1) {
+        double2 *peers[16];
+        for (int r = 0; r < P; ++r) peers[r] = pl->peer_recv[r] + half;
+        return run_passes(pl, pl->passes, in, nullptr, peers, (int64_t)pl->rank * chunk);
+    }
+    ProfScope sc(pl, "pcombine", 32 * M);
+    CUDA_TRY(launch_pcombine(pl->recv + half, out, chunk, P, pl->sign > 0, pl->stream));
+    pl->xbuf ^= 1;
+    return MOA_OK;
+}
+
+int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
+    cudaStream_t s = pl->stream;
+    if (pl->rows) {   // r-D: (FFT Omega) along the last axis, then one pass per other axis, in place
+        pl->rows->stream = s;
+        pl->rows->profiling = pl->profiling;
+        int rc = execute(pl->rows, in, out);
+        if (rc) return rc;
+        for (size_t i = 0; i < pl->passes.size(); ++i) {
+            PassPlan &pp = pl->passes[i];
+            const double2 *src = pp.io == 2 ? pl->work : out;
+            double2 *dst = pp.io == 1 ? pl->work : out;
+            if ((rc = launch_pp(pl, pp, (int)i + 1, src, dst)) != MOA_OK) return rc;
+        }
+        return MOA_OK;
+    }
+    if (pl->mode == MOA_MODE_LITERAL) {
+        // Fig 2.1 literally: (1) x <- P_n x; (2)-(7) t radix-2 stages (Fig 3.9)
+        const int t = pl->t;
+        {
+            ProfScope sc(pl, "bitrev", 32 * pl->n);
+            CUDA_TRY(launch_bitrev(in, pl->work, t, pl->sign > 0, s));
+        }
+        for (int q = 1; q <= t; ++q) {
+            const double2 *src = (q == 1) ? pl->work : out;
+            ProfScope sc(pl, "radix2_stage", 32 * pl->n);
+            CUDA_TRY(launch_radix2_stage(src, out, t, q, pl->tw_hi, pl->tw_lo, pl->hbits,
+                                         (q == t) && pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
+    if (pl->p == 1 && pl->fused) {
+        int rc0 = launch_pp(pl, pl->passes[0], 0, in, pl->work);
+        if (rc0) return rc0;
+        FusedDesc fd = pl->fd;
+        fd.work = pl->work;
+        fd.out = out;
+        fd.epoch = pl->epoch++;
+        char name[64];
+        snprintf(name, sizeof name, "pass1+2 fused<F=%d,T=%d|F=%d,T=%d>", 1 << pl->passes[1].logF,
+                 pl->passes[1].T, 1 << pl->passes[2].logF, pl->passes[2].T);
+        ProfScope sc(pl, name, 32 * pl->M);
+        CUDA_TRY(launch_fused(pl->passes[1].logF, pl->passes[1].T, pl->passes[2].logF, pl->passes[2].T, fd,
+                              pl->fmap2, pl->fmap3, pl->fgrid, s));
+        return MOA_OK;
+    }
+    if (pl->p == 1) return run_passes(pl, pl->passes, in, out);
+
+    const int P = pl->p;
+    const int64_t M = pl->M, chunk = M / P;
+    if (pl->mode == MOA_MODE_EMULATED && pl->exchange != MOA_XCHG_NCCL) {
+        // fused exchange: virtual rank r's last pass stores straight into every
+        // destination's receive block (recv + d*M + r*chunk)
+        double2 *peers[16];
+        for (int dd = 0; dd < P; ++dd) peers[dd] = pl->recv + dd * M;
+        for (int r = 0; r < P; ++r) {
+            int rc = run_passes(pl, pl->rank_passes[r], in + r * M, nullptr, peers, r * chunk);
+            if (rc) return rc;
+        }
+        for (int dd = 0; dd < P; ++dd) {
+            ProfScope sc(pl, "pcombine", 32 * M);
+            CUDA_TRY(launch_pcombine(pl->recv + dd * M, out + dd * M, chunk, P, pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
+    if (pl->mode == MOA_MODE_EMULATED) {
+        for (int r = 0; r < P; ++r) {
+            int rc = run_passes(pl, pl->rank_passes[r], in + r * M, pl->send + r * M);
+            if (rc) return rc;
+        }
+        // S7 emulated: recv_d[s] = send_s[d]  (Fig 5.9 SEND/RECEIVE)
+        for (int dd = 0; dd < P; ++dd)
+            for (int sr = 0; sr < P; ++sr)
+                CUDA_TRY(cudaMemcpyAsync(pl->recv + dd * M + sr * chunk, pl->send + sr * M + dd * chunk,
+                                         chunk * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        for (int dd = 0; dd < P; ++dd) {
+            ProfScope sc(pl, "pcombine", 32 * M);
+            CUDA_TRY(launch_pcombine(pl->recv + dd * M, out + dd * M, chunk, P, pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
+    if (pl->exchange != MOA_XCHG_NCCL) {
+        if (pl->exchange == MOA_XCHG_P2P_EXTERNAL)
+            return fail(MOA_ERR_INVALID_ARG, "P2P_EXTERNAL plans run through moa_fft_execute_phase");
+        if (!pl->peers_open) return fail(MOA_ERR_INVALID_ARG, "P2P plan without peers (moa_fft_enable_p2p)");
+        int rc = p2p_phase(pl, in, out, 1);
+        if (rc) return rc;
+        std::string err;
+        {
+            ProfScope sc(pl, "barrier (NCCL 8 B)", 0);
+            rc = dist_barrier(s, &err);
+        }
+        if (rc) return fail(rc, "%s", err.c_str());
+        return p2p_phase(pl, in, out, 2);
+    }
+    int rc = run_passes(pl, pl->passes, in, pl->send);
+    if (rc) return rc;
+    std::string err;
+    {
+        ProfScope sc(pl, "alltoall (NCCL)", 16 * chunk * (P - 1));
+        rc = dist_alltoall(pl->send, pl->recv, chunk, P, pl->rank, s, &err);
+    }
+    if (rc) return fail(rc, "%s", err.c_str());
+    ProfScope sc(pl, "pcombine", 32 * M);
+    CUDA_TRY(launch_pcombine(pl->recv, out, chunk, P, pl->sign > 0, s));
+    return MOA_OK;
+}
+
+}  // namespace moa
