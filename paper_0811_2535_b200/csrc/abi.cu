@@ -42,7 +42,8 @@ int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != pl->device) cudaSetDevice(pl->device);
-    int rc = execute(pl, (const double2 *)in, (double2 *)out);
+    int rc = (pl->graph_ok && !pl->profiling) ? execute_graph(pl, (const double2 *)in, (double2 *)out)
+                                              : execute(pl, (const double2 *)in, (double2 *)out);
     if (cur != pl->device) cudaSetDevice(cur);
     return rc;
 }

@@ -215,4 +215,54 @@ int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
     return MOA_OK;
 }
 
+// Replay the plan's launches as one CUDA graph.  The first execute with a given
+// (in, out) captures them on a private stream (the kernels and their programmatic
+// dependencies become graph nodes); later executes with the same pointers launch the
+// instantiated graph on the plan stream with one call, which removes the per-kernel
+// CPU submission from small, latency-bound transforms.  A different (in, out) pair
+// re-captures.
+int execute_graph(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
+    if (pl->gexec && pl->g_in == (const void *)in && pl->g_out == (void *)out) {
+        CUDA_TRY(cudaGraphLaunch(pl->gexec, pl->stream));
+        return MOA_OK;
+    }
+    if (!pl->graph_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->graph_stream, cudaStreamNonBlocking));
+    cudaStream_t user = pl->stream;
+    pl->stream = pl->graph_stream;
+    cudaGraph_t g = nullptr;
+    int rc = MOA_OK;
+    cudaError_t e = cudaStreamBeginCapture(pl->graph_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        rc = execute(pl, in, out);
+        e = cudaStreamEndCapture(pl->graph_stream, &g);
+    }
+    pl->stream = user;
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        pl->graph_ok = false;   // capture unsupported here: plain launches from now on
+        return execute(pl, in, out);
+    }
+    if (pl->gexec) {
+        cudaGraphExecDestroy(pl->gexec);
+        pl->gexec = nullptr;
+    }
+    e = cudaGraphInstantiate(&pl->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        pl->gexec = nullptr;
+        pl->graph_ok = false;
+        return execute(pl, in, out);
+    }
+    pl->g_in = in;
+    pl->g_out = out;
+    CUDA_TRY(cudaGraphLaunch(pl->gexec, pl->stream));
+    return MOA_OK;
+}
+
 }  // namespace moa

@@ -421,6 +421,8 @@ void free_plan(moa_fft_plan_s *pl) {
     cudaFree(pl->items);
     cudaFree(pl->counters);
     cudaFree(pl->scratch);
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    if (pl->graph_stream) cudaStreamDestroy(pl->graph_stream);
     for (auto &r : pl->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -665,6 +667,10 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
             return rc;
         }
     }
+    // graph replay: single-GPU lifted plans whose launches do not change between
+    // executes (the fused kernel's epoch counter does; p > 1 alternates buffers)
+    // (measured: 2^14-2^18 -1 us, 2^24 271.4 -> 268.3 us; a one-kernel plan gains nothing)
+    pl->graph_ok = p == 1 && mode == MOA_MODE_LIFTED && !pl->fused && pl->d >= 2 && env_int("MOA_FFT_GRAPH", 1);
     *res = pl;
     return MOA_OK;
 }

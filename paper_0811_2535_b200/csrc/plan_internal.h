@@ -106,6 +106,14 @@ struct moa_fft_plan_s {
     unsigned long long *counters = nullptr;
     double2 *scratch = nullptr;
     unsigned long long epoch = 0;
+    // CUDA-graph replay of execute (single-GPU plans): the launches of one execute for
+    // the last (in, out) pair, captured on a private stream, replayed with one
+    // cudaGraphLaunch on the plan stream
+    bool graph_ok = false;
+    cudaStream_t graph_stream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    const void *g_in = nullptr;
+    void *g_out = nullptr;
     // per-kernel event profiling (moa_fft_set_profiling)
     bool profiling = false;
     struct Slot {
@@ -143,5 +151,6 @@ int run_passes(moa_fft_plan_s *pl, std::vector<PassPlan> &ps, const double2 *in,
                double2 *const *peers = nullptr, int64_t peer_off = 0);
 int p2p_phase(moa_fft_plan_s *pl, const double2 *in, double2 *out, int phase);
 int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out);
+int execute_graph(moa_fft_plan_s *pl, const double2 *in, double2 *out);
 
 }  // namespace moa

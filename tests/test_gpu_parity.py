@@ -87,6 +87,29 @@ def test_inplace_equals_out_of_place_bitwise(t):
     assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
+def test_graph_replay_matches_plain_launches(monkeypatch):
+    """Executes replay a captured CUDA graph per (in, out) pair: repeated, alternating and
+    in-place executes are bitwise equal to plans that launch kernel by kernel."""
+    t = 18
+    x1 = _dev(moa_inputs.signal_for(t))
+    x2 = _dev(moa_inputs.complex_signal(moa_inputs.seed_for(t) + 5, 1 << t))
+    g = moa.Plan(1 << t)
+    monkeypatch.setenv("MOA_FFT_GRAPH", "0")
+    plain = moa.Plan(1 << t)
+    refs = [plain.execute(x1), plain.execute(x2)]
+    o1, o2 = torch.empty_like(x1), torch.empty_like(x1)
+    for _ in range(3):
+        for x, o, ref in ((x1, o1, refs[0]), (x2, o2, refs[1]), (x1, o2, refs[0])):
+            g.execute(x, o)
+            torch.cuda.synchronize()
+            assert torch.equal(o, ref)
+    y = x2.clone()
+    g.execute(y, y)
+    g.execute(x2, x2.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(y, refs[1])
+
+
 def test_input_not_modified():
     x = moa_inputs.signal_for(16)
     xd = _dev(x)
