@@ -17,7 +17,7 @@ import os
 
 from . import build as _build
 
-__all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "scatter_cyclic", "gather_cyclic", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
+__all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "dist_fft", "scatter_cyclic", "gather_cyclic", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
            "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
@@ -388,6 +388,24 @@ def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
     if rc:
         _err(rc)
     return int(F.value), a, b, c
+
+
+def dist_fft(x_local, n: int, sign: int = -1, out=None, exchange: int = XCHG_NCCL):
+    """One partitioned n-point transform over the torch.distributed world (after dist_init):
+    x_local = x[rank::p] (complex128, this rank's GPU) -> X[rank::p] (the paper's xcyclic,
+    P:799).  Collective: every rank calls it.  exchange = XCHG_P2P fuses the
+    all-to-all into the last pass (the plan maps the peers' buffers first)."""
+    import torch
+    import torch.distributed as dist
+    p = dist.get_world_size()
+    plan = Plan(n, p, sign, exchange=exchange)
+    try:
+        if exchange == XCHG_P2P:
+            plan.enable_p2p()
+        return plan.execute(x_local.contiguous(), out)
+    finally:
+        torch.cuda.current_stream().synchronize()
+        plan.destroy()
 
 
 def scatter_cyclic(x0, n: int, group=None, device=None):
