@@ -278,6 +278,27 @@ __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 
     }
 }
 
+// The first stage's gather of `tile` into registers (lane mapping of the SRC 0 stage).
+template <int F, int T>
+__device__ __forceinline__ void rdb_load_tile(double2 *x, const PassDesc &d, const TileIO &io, int64_t b) {
+    using SH = PassShape<F, T>;
+    constexpr int RS = F >= MOA_RMAX ? MOA_RMAX : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
+    const int64_t u = b & (d.U - 1);
+    const int64_t v = (b >> d.lU) & (d.V - 1);
+    const int64_t w = b >> (d.lU + d.lV);
+    const double2 *in = io.src + (u * d.in_u + v * d.in_v + w * d.in_w - io.in_shift);
+    const uint32_t sf = (uint32_t)NB * (uint32_t)d.in_f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const int bb = threadIdx.x + NT * i;
+        const bool tfast = T > 1 && d.in_tfast;
+        const int t = tfast ? bb % T : bb / NB, j = tfast ? bb / T : bb % NB;
+        const double2 *p = elem_off(in, (uint32_t)t * (uint32_t)d.in_t + (uint32_t)j * (uint32_t)d.in_f);
+#pragma unroll
+        for (int r = 0; r < RS; ++r) x[i * RS + r] = __ldg(elem_off_c(p, r, sf));
+    }
+}
+
 // One Stockham stage: Ns = product of the radices already applied.
 //   SRC 0: the first stage gathers from global memory; SRC 1/2: from the TMA
 //   staging buffer `inbuf`, after which hook() runs (barrier + next prefetch).
@@ -338,6 +359,17 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         }
         if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
+    } else if constexpr (FIRST && SRC == 6) {
+        // register double buffering (fft_pass_rdb_kernel): this tile's points were loaded
+        // into the hook's registers during the previous tile; take them and start the
+        // loads of the CTA's next tile into the same registers at once
+        hook.take(x);
+        hook.prefetch();
+        if (d.conj_in) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
+        }
+        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
     } else if constexpr (FIRST && SRC == 3) {
         // prefetched by this same thread (cp.async, fft_pass_pf_kernel) into the
         // exchange layout: its own copies are visible after cp.async.wait_all
@@ -558,6 +590,66 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register double buffering: a persistent CTA holds the NEXT tile's points in a second
+// register set; the loads for tile i+1 are issued as soon as tile i's points have been
+// taken out of it, so they overlap all of tile i's butterflies, exchange and stores.
+// 3 CTAs/SM (<= 170 registers: two 16-point sets per thread).
+template <int F, int T>
+struct RdbHook {
+    double2 *nx;   // PassShape<F,T>::R registers (fully unrolled, never indexed dynamically)
+    const PassDesc *d;
+    const TileIO *io;
+    int64_t next, tiles;
+    __device__ __forceinline__ void take(double2 *x) const {
+#pragma unroll
+        for (int k = 0; k < PassShape<F, T>::R; ++k) x[k] = nx[k];
+    }
+    __device__ __forceinline__ void prefetch() const {
+        if (next < tiles) rdb_load_tile<F, T>(nx, *d, *io, next);
+    }
+    __device__ __forceinline__ void operator()() const {}
+};
+
+template <int F, int T>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, 3) fft_pass_rdb_kernel(const PassDesc d, int64_t tiles) {
+    extern __shared__ double2 sm[];
+    double2 *tw = reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    int64_t tile = blockIdx.x;
+    if (tile >= tiles) return;
+    double2 nx[PassShape<F, T>::R];
+    rdb_load_tile<F, T>(nx, d, io, tile);
+    for (; tile < tiles; tile += gridDim.x) {
+        const RdbHook<F, T> hk{nx, &d, &io, tile + (int64_t)gridDim.x, tiles};
+        tile_fft<F, T, 6, RdbHook<F, T>>(sm, tw, d, io, tile, nullptr, hk);
+        __syncthreads();   // every lane is done with the exchange buffer and the tables
+    }
+}
+
+template <int F, int T>
+cudaError_t launch_one_rdb(const PassDesc &d, int64_t tiles, int grid, cudaStream_t s) {
+    using SH = PassShape<F, T>;
+    fft_pass_rdb_kernel<F, T><<<grid, SH::NT, SH::SMEM, s>>>(d, tiles);
+    return cudaGetLastError();
+}
+
+template <int F, int T>
+int grid_one_rdb() {
+    using SH = PassShape<F, T>;
+    if (SH::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(fft_pass_rdb_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM) !=
+            cudaSuccess)
+        return 0;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft_pass_rdb_kernel<F, T>, SH::NT, SH::SMEM) !=
+        cudaSuccess)
+        return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
+}
+
 // persistent plain pass: the tile loop of fft_pass_kernel without CTA turnover
 template <int F, int T>
 __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
@@ -574,11 +666,12 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
 template <int F, int T>
 cudaError_t launch_one_pf(const PassDesc &d, int64_t tiles, int grid, cudaStream_t s) {
     using SH = PassShape<F, T>;
-    static const int persist = [] {
+    static const int pf_kind = [] {
         const char *e = getenv("MOA_FFT_PF");
-        return e && atoi(e) == 2;
+        return e ? atoi(e) : 0;
     }();
-    if (persist) {
+    if (pf_kind == 3) return launch_one_rdb<F, T>(d, tiles, grid, s);
+    if (pf_kind == 2) {
         if (SH::SMEM > 48 * 1024)
             cudaFuncSetAttribute(fft_pass_persist_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SH::SMEM);
@@ -592,6 +685,8 @@ cudaError_t launch_one_pf(const PassDesc &d, int64_t tiles, int grid, cudaStream
 template <int F, int T>
 int grid_one_pf() {
     using SH = PassShape<F, T>;
+    const char *e = getenv("MOA_FFT_PF");
+    if (e && atoi(e) == 3) return grid_one_rdb<F, T>();
     if (SH::SMEM > 48 * 1024 &&
         cudaFuncSetAttribute(fft_pass_pf_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM) !=
             cudaSuccess)

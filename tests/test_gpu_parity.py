@@ -175,7 +175,7 @@ def test_plan_info():
     assert info["passes"] == 4 and info["lift"] == [64, 128, 256, 256]
 
 
-@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_PF": "1"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "2"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
+@pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_PF": "1"}, {"MOA_FFT_PF": "3"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "2"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
 def test_variant_kernels_parity(env, monkeypatch):
     """The L2-fused last passes and the TMA-staged passes (env-selected variants)."""
     for k, v in env.items():
