@@ -238,8 +238,10 @@ def run_ours(args, rank: int, world: int):
             if cand is not None:
                 cand.destroy()
     exchange_used = "p2p" if plan is not None else "nccl"
+    t_plan0 = time.perf_counter()
     if plan is None:
         plan = moa.Plan(n, world, -1, stream=stream)
+    plan_ms = (time.perf_counter() - t_plan0) * 1e3   # plan creation: outside the timed region
     args.exchange = exchange_used
     info = plan.info()
     lib = moa.load()
@@ -355,6 +357,7 @@ def run_ours(args, rank: int, world: int):
                         "frac_of_measured": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9
                                                   / peaks["hbm_gbs"], 4)},
                 "roofline": roofline, "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e,
+                "plan_ms": round(plan_ms, 2),
                 "gpu_launches": int(args.steps * info["launches"]),
                 "clocks": sampler.summary()}
         if world > 1:
