@@ -155,6 +155,10 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
  *           in[j] = x[rank + p*j], out[i] = X[rank + p*i] (the paper's xcyclic,
  *           P:799).  Collective: every rank calls it in the same order.
  *   EMULATED plans: in/out hold all p ranks' slices back to back (p*(n/p)).
+ * Single-GPU multi-pass plans replay their kernel launches as one CUDA graph per
+ * (in, out) pair: the first execute with a new pair captures it (on a private
+ * stream) and launches it; the graph only remembers the pointer values, so the
+ * caller may free or reuse the buffers afterwards ($MOA_FFT_GRAPH=0 disables it).
  * Returns MOA_OK or MOA_ERR_ALIGN / MOA_ERR_CUDA / MOA_ERR_NCCL.
  */
 int moa_fft_execute(moa_fft_plan_t plan, const void *in, void *out);
