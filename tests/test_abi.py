@@ -102,3 +102,18 @@ def test_p2p_calls_reject_non_p2p_plans():
     assert lib.moa_fft_enable_p2p(None) == -9
     assert lib.moa_fft_execute_phase(None, None, None, 1) == -9
     assert lib.moa_fft_execute_host_batch(None, 0, None, None) == -9
+
+
+@pytest.mark.parametrize("shape,needle", [
+    ((4,), "rank 1 must be 2 or 3"),
+    ((2, 2, 2, 2), "rank 4 must be 2 or 3"),
+    ((3, 8), "n1=3 must be 2^t"),
+    ((1 << 27, 4), "<= 26"),
+    ((8, 6), "n2=6 must be 2^t"),
+    ((1 << 16, 1 << 17), "more than 2^32"),
+])
+def test_nd_plan_validation_errors(shape, needle):
+    """r-D plan checks run before any device call (CPU-testable)."""
+    with pytest.raises(moa.MoaError) as e:
+        moa.PlanND(shape)
+    assert needle in str(e.value), str(e.value)
