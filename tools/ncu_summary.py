@@ -19,7 +19,7 @@ names = [n for n in a.names.split(";") if n]
 def g(r, k):
     return r[hdr.index(k)] if k in hdr else ""
 lines = [f"# ncu summary: {os.path.basename(a.rep)}", "",
-         "| # | kernel | dur (us) | DRAM read (MB) | DRAM write (MB) | DRAM % peak | issue % | warps % | regs | grid | top stalls |",
+         "| # | kernel | duration | DRAM read (MB) | DRAM write (MB) | DRAM % peak | issue % | warps % | regs | grid | top stalls |",
          "|---|---|---|---|---|---|---|---|---|---|---|"]
 traffic_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
 try:
@@ -41,7 +41,7 @@ for i, r in enumerate(rows[2:]):
     ur, uw = units[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_write.sum")]
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
     rd_mb, wr_mb = rd * scale.get(ur, 1), wr * scale.get(uw, 1)
-    lines.append(f"| {i} | `{g(r, 'Kernel Name')[:70]}` | {g(r, 'gpu__time_duration.sum')} | {rd_mb:.1f} | {wr_mb:.1f} | "
+    lines.append(f"| {i} | `{g(r, 'Kernel Name')[:70]}` | {g(r, 'gpu__time_duration.sum')} {units[hdr.index('gpu__time_duration.sum')]} | {rd_mb:.1f} | {wr_mb:.1f} | "
                  f"{float(g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed') or 0):.1f} | "
                  f"{float(g(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
                  f"{float(g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
