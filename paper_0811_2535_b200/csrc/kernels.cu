@@ -208,27 +208,45 @@ cudaError_t launch_radix2_stage(const double2 *in, double2 *out, int t, int q, c
 // The paper's stages q = breakpoint..t with weightcyclic (Fig 5.7) are,
 // after that twiddle, the P-point DFT  out_d[c + chunk*k2] = sum_s omega_P^(s*k2) R_d[s][c].
 template <int P>
-__global__ void pcombine_kernel(const double2 *__restrict__ recv, double2 *__restrict__ out, int64_t chunk,
-                                int conj_out) {
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < chunk;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        double2 v[P];
+__global__ void __launch_bounds__(256) pcombine_kernel(const double2 *__restrict__ recv, double2 *__restrict__ out,
+                                                       int64_t chunk, int conj_out) {
+    // U columns c per thread, all loads issued before any DFT (memory-level
+    // parallelism of a streaming pass: P*U independent 16-byte loads in flight)
+    constexpr int U = P >= 8 ? 2 : 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < chunk; c0 += U * stride) {
+        double2 v[U][P];
 #pragma unroll
-        for (int s = 0; s < P; ++s) v[s] = __ldg(recv + s * chunk + c);
-        dft_reg<P>(v);
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + u * stride;
+            if (c < chunk) {
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            double2 o = v[k];
-            if (conj_out) o.y = -o.y;
-            out[c + chunk * k] = o;
+                for (int s = 0; s < P; ++s) v[u][s] = __ldg(recv + s * chunk + c);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + u * stride;
+            if (c >= chunk) break;
+            dft_reg<P>(v[u]);
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                double2 o = v[u][k];
+                if (conj_out) o.y = -o.y;
+                __stcs(out + c + chunk * k, o);
+            }
         }
     }
 }
 
 cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, int P, int conj_out,
                             cudaStream_t s) {
+    // one wave of 8 CTAs of 256 threads per SM, each thread U columns per sweep
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = (chunk + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     switch (P) {
     case 2: pcombine_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, conj_out); break;
     case 4: pcombine_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, conj_out); break;
