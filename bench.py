@@ -274,6 +274,19 @@ def run_ours(args, rank: int, world: int):
     barrier()
     elapsed = ev0.elapsed_time(ev1) * 1e-3
 
+    # ---- per-step spread (median / min / max) from K more steps with an event between steps
+    step_evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    step_evs[0].record(stream)
+    for i in range(args.steps):
+        plan.execute(x, out)
+        step_evs[i + 1].record(stream)
+    step_evs[-1].synchronize()
+    step_ms = sorted(step_evs[i].elapsed_time(step_evs[i + 1]) for i in range(args.steps))
+    step_stats = {"median": round(statistics.median(step_ms), 4), "min": round(step_ms[0], 4),
+                  "max": round(step_ms[-1], 4)}
+
     # ---- the same K steps again with an event pair around every kernel (moa_fft_set_profiling):
     # per-kernel durations for the roofline line
     lib.moa_fft_set_profiling(plan._h, 1)
@@ -357,7 +370,7 @@ def run_ours(args, rank: int, world: int):
                         "frac_of_measured": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9
                                                   / peaks["hbm_gbs"], 4)},
                 "roofline": roofline, "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e,
-                "plan_ms": round(plan_ms, 2),
+                "plan_ms": round(plan_ms, 2), "step_ms": step_stats,
                 "gpu_launches": int(args.steps * info["launches"]),
                 "clocks": sampler.summary()}
         if world > 1:
