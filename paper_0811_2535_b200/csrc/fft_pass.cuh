@@ -147,8 +147,23 @@ __device__ __forceinline__ int smem_idx(int t, int f) {
     return t * (F + PAD) + (f ^ s);
 }
 
-// radix of the last Stockham stage of an F-point transform (radix 16 first, remainder last)
+// Radix of the Stockham stage that starts once NS points have been combined.
+// F <= 256 or a power of 16: radix 16 first, the remainder last.  F >= 512 otherwise:
+// the remainder FIRST, then radix 16, so the last stage is radix 16 and the per-tile
+// pass-twiddle table holds F/16 entries per transform instead of F/2 .. F/8.
+__host__ __device__ constexpr int first_radix(int F) {
+    int r = F;
+    while (r > MOA_RMAX) r /= MOA_RMAX;
+    return r;
+}
+__host__ __device__ constexpr bool remainder_first(int F) { return F >= 512 && first_radix(F) != MOA_RMAX; }
+__host__ __device__ constexpr int stage_radix(int F, int NS) {
+    if (remainder_first(F)) return NS == 1 ? first_radix(F) : MOA_RMAX;
+    return F / NS >= MOA_RMAX ? MOA_RMAX : F / NS;
+}
+// radix of the last stage
 __host__ __device__ constexpr int lrs(int F) {
+    if (remainder_first(F)) return MOA_RMAX;
     int ns = 1;
     while (F / ns > MOA_RMAX) ns *= MOA_RMAX;
     return F / ns;
@@ -282,7 +297,7 @@ __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 
 template <int F, int T>
 __device__ __forceinline__ void rdb_load_tile(double2 *x, const PassDesc &d, const TileIO &io, int64_t b) {
     using SH = PassShape<F, T>;
-    constexpr int RS = F >= MOA_RMAX ? MOA_RMAX : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
+    constexpr int RS = stage_radix(F, 1), NB = F / RS, M = SH::R / RS, NT = SH::NT;
     const int64_t u = b & (d.U - 1);
     const int64_t v = (b >> d.lU) & (d.V - 1);
     const int64_t w = b >> (d.lU + d.lV);
@@ -313,7 +328,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     constexpr int R = SH::R;
     constexpr int NT = SH::NT;
     constexpr int REM = F / NS;
-    constexpr int RS = REM >= MOA_RMAX ? MOA_RMAX : REM;   // radix of this stage
+    constexpr int RS = stage_radix(F, NS);   // radix of this stage
     constexpr int NB = F / RS;                 // butterflies per transform
     constexpr int M = R / RS;                  // butterflies per thread
     constexpr bool LAST = (NS * RS == F);
@@ -474,8 +489,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
 __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
                                            const double2 *inbuf, const Hook &hook) {
-    constexpr int REM = F / NS;
-    constexpr int RS = REM >= MOA_RMAX ? MOA_RMAX : REM;
+    constexpr int RS = stage_radix(F, NS);
     fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
     if constexpr (NS * RS < F) fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
 }
@@ -542,7 +556,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int F, int T>
 __device__ __forceinline__ void prefetch_tile(double2 *sm, const PassDesc &d, const TileIO &io, int64_t b) {
     using SH = PassShape<F, T>;
-    constexpr int RS = F >= MOA_RMAX ? MOA_RMAX : F, NB = F / RS, M = SH::R / RS, NT = SH::NT;
+    constexpr int RS = stage_radix(F, 1), NB = F / RS, M = SH::R / RS, NT = SH::NT;
     const int64_t u = b & (d.U - 1);
     const int64_t v = (b >> d.lU) & (d.V - 1);
     const int64_t w = b >> (d.lU + d.lV);
