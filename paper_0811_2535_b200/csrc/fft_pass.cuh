@@ -148,15 +148,18 @@ __device__ __forceinline__ int smem_idx(int t, int f) {
 }
 
 // Radix of the Stockham stage that starts once NS points have been combined.
-// F <= 256 or a power of 16: radix 16 first, the remainder last.  F >= 512 otherwise:
-// the remainder FIRST, then radix 16, so the last stage is radix 16 and the per-tile
-// pass-twiddle table holds F/16 entries per transform instead of F/2 .. F/8.
+// F a power of 16 (or < 32): radix 16 throughout.  Otherwise the remainder FIRST, then
+// radix 16, so the last stage is radix 16 and the per-tile pass-twiddle table holds F/16
+// entries per transform (measured faster than remainder-last at every F).
 __host__ __device__ constexpr int first_radix(int F) {
     int r = F;
     while (r > MOA_RMAX) r /= MOA_RMAX;
     return r;
 }
-__host__ __device__ constexpr bool remainder_first(int F) { return F >= 512 && first_radix(F) != MOA_RMAX; }
+#ifndef MOA_RF_MIN
+#define MOA_RF_MIN 32
+#endif
+__host__ __device__ constexpr bool remainder_first(int F) { return F >= MOA_RF_MIN && first_radix(F) != MOA_RMAX; }
 __host__ __device__ constexpr int stage_radix(int F, int NS) {
     if (remainder_first(F)) return NS == 1 ? first_radix(F) : MOA_RMAX;
     return F / NS >= MOA_RMAX ? MOA_RMAX : F / NS;
