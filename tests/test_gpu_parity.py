@@ -77,6 +77,39 @@ def test_lifted_explicit_liftings(t, lift):
     assert oracle.rel_l2(got, ref) <= tol(t), lift
 
 
+def _random_liftings(seed=0x11F7, per_t=3):
+    """Seeded random factorisations of 2^t into 1-4 powers of two in [2, 2^13]."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for t in range(2, 23):
+        seen = set()
+        for _ in range(12):
+            d = int(rng.integers(1, 5))
+            if d > t or (d == 1 and t > 13):
+                continue
+            cuts = sorted(rng.choice(np.arange(1, t), size=d - 1, replace=False)) if d > 1 else []
+            bits = np.diff([0, *cuts, t])
+            if any(b > 13 for b in bits):
+                continue
+            lift = tuple(int(1 << b) for b in bits)
+            if lift not in seen:
+                seen.add(lift)
+                cases.append((t, list(lift)))
+            if len(seen) >= per_t:
+                break
+    return cases
+
+
+@pytest.mark.parametrize("t,lift", _random_liftings())
+def test_random_liftings(t, lift):
+    """Any valid lifting <F1..Fd> (the paper's 'not necessary blocked in squares')
+    gives the same transform: seeded random factorisations, both signs."""
+    x = moa_inputs.signal_for(t)
+    for sign in (-1, 1):
+        got = _run(moa.Plan(1 << t, 1, sign, lift=lift), x)
+        assert oracle.rel_l2(got, oracle.fft(x, sign, threads=8)) <= tol(t), (t, lift, sign)
+
+
 @pytest.mark.parametrize("t", [3, 10, 14, 20])
 def test_inplace_equals_out_of_place_bitwise(t):
     x = moa_inputs.signal_for(t)
