@@ -84,7 +84,10 @@ def main():
             f.write(f"Median of 20 (t <= 26) or 5 executes; L2 flushed (1 GiB write) before each 'cold' "
                     f"execute, none before 'hot'. GFLOP/s = 5 n log2 n / t. alg GB/s = 32 n x HBM passes / t; "
                     f"fraction of the measured {pk} GB/s copy peak (MEASURED_PEAKS.json). Sizes <= 2^13 run "
-                    f"in one CTA (latency-bound); up to ~2^22 the data is L2-resident between passes.\n\n")
+                    f"in one CTA (latency-bound); up to ~2^22 the data is L2-resident between passes. "
+                    f"For launch-bound sizes the 'hot' column includes the CPU submission latency (the GPU "
+                    f"is idle when the transform is launched), while in the 'cold' column the preceding flush "
+                    f"kernel hides it.\n\n")
             f.write("| t | lifting | launches | us (cold) | us (hot) | GFLOP/s (cold) | GFLOP/s (hot) | alg GB/s | "
                     "frac HBM |\n|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
