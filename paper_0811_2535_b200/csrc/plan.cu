@@ -215,6 +215,14 @@ int choose_T(int logF, int64_t avail) {
     return T;
 }
 
+// Small transforms: halve T while the pass would have fewer than ~one tile per SM
+// (measured: 2^18 <512,512> 18.5 -> 16.4 us), keeping T >= 2 for the column runs.
+static int fill_T(int T, int64_t transforms, int64_t batch) {
+    const int64_t min_tiles = env_int("MOA_FFT_MINTILES", 128);
+    while (T > 2 && transforms * batch / T < min_tiles) T /= 2;
+    return T;
+}
+
 // Build the passes of a local FFT of length M = prod(lift) (global length n).
 // rank >= 0 with P > 1: the last pass scales by omega_n^(rank*K) and packs to
 // the send layout [dst][c] with K = dst + P*c (S6, fused into S4's epilogue).
@@ -244,7 +252,7 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
         if (i < d - 1) {
             // middle pass: view [A][F][B], F-point DFTs along the middle axis for
             // every (a, b); twiddle omega_{F*B}^(b*k) = omega_n^(b*k*n/(F*B)); in place.
-            int T = choose_T(pp.logF, B);
+            int T = fill_T(choose_T(pp.logF, B), pl->M / F, pl->batch);
             pp.T = T;
             D.U = B / T;
             D.V = A;
@@ -314,7 +322,7 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
                 D.pack_chunk = pl->M / P;
                 pp.tiles = D.U * D.V * (d >= 3 ? Fv[1] : 1);
             } else {
-                int T = choose_T(pp.logF, Fv[0]);
+                int T = fill_T(choose_T(pp.logF, Fv[0]), pl->M / F, pl->batch);
                 pp.T = T;
                 D.U = Fv[0] / T;
                 D.V = d >= 3 ? Fv[1] : 1;
