@@ -157,7 +157,7 @@ void choose_tma(PassPlan &pp) {
 // on (two <= 128-point column passes instead of one long one).  p > 1 plans keep <= 3
 // levels.
 int default_lifting(int tl, int64_t *lift, int p) {
-    if (tl <= FMAX_LOG) {
+    if (tl <= 12) {   // one CTA per transform (2^13 in one CTA: 18.4 us, as <64,128>: 12.3 us)
         lift[0] = (int64_t)1 << tl;
         return 1;
     }
