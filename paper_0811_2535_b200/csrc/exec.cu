@@ -4,6 +4,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <vector>
+
 #include "plan_internal.h"
 
 namespace moa {
@@ -172,6 +174,36 @@ int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
         }
         return MOA_OK;
     }
+    if (pl->mode == MOA_MODE_EMULATED && pl->chunks > 1) {
+        // chunked exchange on virtual ranks: same group passes, per-chunk copies, chunk combine
+        const int G = pl->chunks;
+        const int64_t cnt = M / ((int64_t)G * P);
+        for (int r = 0; r < P; ++r) {
+            std::vector<PassPlan> &ps = pl->rank_passes[r];
+            for (size_t i = 0; i + 1 < ps.size(); ++i) {
+                int rc = launch_pp(pl, ps[i], (int)i, i == 0 ? in + r * M : pl->work, pl->work);
+                if (rc) return rc;
+            }
+            for (int g = 0; g < G; ++g) {
+                int rc = launch_pp(pl, pl->rank_chunk_last[r][g], (int)ps.size() - 1, pl->work, pl->send + r * M);
+                if (rc) return rc;
+            }
+        }
+        for (int g = 0; g < G; ++g)
+            for (int dd = 0; dd < P; ++dd)
+                for (int sr = 0; sr < P; ++sr)
+                    CUDA_TRY(cudaMemcpyAsync(pl->recv + dd * M + g * (M / G) + sr * cnt,
+                                             pl->send + sr * M + g * (M / G) + dd * cnt, cnt * sizeof(double2),
+                                             cudaMemcpyDeviceToDevice, s));
+        const int64_t F0 = pl->lift[0], F1 = pl->lift[1];
+        for (int dd = 0; dd < P; ++dd)
+            for (int g = 0; g < G; ++g) {
+                ProfScope sc(pl, "pcombine_chunk", 32 * M / G);
+                CUDA_TRY(launch_pcombine_chunk(pl->recv + dd * M + g * (M / G), out + dd * M, cnt, P, F0 / P, F1 / G,
+                                               F1, g * (F1 / G), chunk, pl->sign > 0, s));
+            }
+        return MOA_OK;
+    }
     if (pl->mode == MOA_MODE_EMULATED) {
         for (int r = 0; r < P; ++r) {
             int rc = run_passes(pl, pl->rank_passes[r], in + r * M, pl->send + r * M);
@@ -201,6 +233,35 @@ int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
         }
         if (rc) return fail(rc, "%s", err.c_str());
         return p2p_phase(pl, in, out, 2);
+    }
+    if (pl->chunks > 1) {
+        // SURVEY §8(e) pipeline: group g's pass (plan stream) -> its all-to-all (comm
+        // stream) -> its combine (side stream); the pass of group g+1 overlaps the
+        // exchange of group g, which overlaps the combine of group g-1
+        const int G = pl->chunks;
+        const int64_t cnt = M / ((int64_t)G * P);
+        const int64_t F0 = pl->lift[0], F1 = pl->lift[1];
+        std::vector<PassPlan> &ps = pl->passes;
+        for (size_t i = 0; i + 1 < ps.size(); ++i) {
+            int rc = launch_pp(pl, ps[i], (int)i, i == 0 ? in : pl->work, pl->work);
+            if (rc) return rc;
+        }
+        std::string err;
+        for (int g = 0; g < G; ++g) {
+            int rc = launch_pp(pl, pl->chunk_last[g], (int)ps.size() - 1, pl->work, pl->send);
+            if (rc) return rc;
+            CUDA_TRY(cudaEventRecord(pl->ev_pass[g], s));
+            CUDA_TRY(cudaStreamWaitEvent(pl->comm_stream, pl->ev_pass[g], 0));
+            rc = dist_alltoall(pl->send + g * (M / G), pl->recv + g * (M / G), cnt, P, pl->rank, pl->comm_stream, &err);
+            if (rc) return fail(rc, "%s", err.c_str());
+            CUDA_TRY(cudaEventRecord(pl->ev_a2a[g], pl->comm_stream));
+            CUDA_TRY(cudaStreamWaitEvent(pl->comb_stream, pl->ev_a2a[g], 0));
+            CUDA_TRY(launch_pcombine_chunk(pl->recv + g * (M / G), out, cnt, P, F0 / P, F1 / G, F1, g * (F1 / G), chunk,
+                                           pl->sign > 0, pl->comb_stream));
+        }
+        CUDA_TRY(cudaEventRecord(pl->ev_comb, pl->comb_stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_comb, 0));
+        return MOA_OK;
     }
     int rc = run_passes(pl, pl->passes, in, pl->send);
     if (rc) return rc;

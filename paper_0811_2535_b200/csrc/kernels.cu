@@ -257,6 +257,48 @@ cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, in
     return cudaGetLastError();
 }
 
+// Chunked form (SURVEY §8(e) overlap): chunk g of the receive buffer, [src][count],
+// column c_local -> global column c = inner_len*(goff + (o % wg) + f1*(o / wg)) + i.
+template <int P>
+__global__ void __launch_bounds__(256) pcombine_chunk_kernel(const double2 *__restrict__ recv,
+                                                             double2 *__restrict__ out, int64_t count, int li,
+                                                             int lwg, int64_t f1, int64_t goff,
+                                                             int64_t out_stride, int conj_out) {
+    for (int64_t cl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cl < count;
+         cl += (int64_t)gridDim.x * blockDim.x) {
+        double2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) v[s] = __ldg(recv + s * count + cl);
+        dft_reg<P>(v);
+        const int64_t i = cl & ((1ll << li) - 1), o = cl >> li;
+        const int64_t c = ((goff + (o & ((1ll << lwg) - 1)) + f1 * (o >> lwg)) << li) + i;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double2 w = v[k];
+            if (conj_out) w.y = -w.y;
+            __stcs(out + c + out_stride * k, w);
+        }
+    }
+}
+
+cudaError_t launch_pcombine_chunk(const double2 *recv, double2 *out, int64_t count, int P, int64_t inner_len,
+                                  int64_t wg, int64_t f1, int64_t goff, int64_t out_stride, int conj_out,
+                                  cudaStream_t s) {
+    int li = 0, lwg = 0;
+    while (((int64_t)1 << li) < inner_len) ++li;
+    while (((int64_t)1 << lwg) < wg) ++lwg;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    switch (P) {
+    case 2: pcombine_chunk_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
+    case 4: pcombine_chunk_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
+    case 8: pcombine_chunk_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
+    case 16: pcombine_chunk_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ input generator (harness)
 __device__ __forceinline__ double splitmix_u(uint64_t seed, uint64_t idx) {
     uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ull;

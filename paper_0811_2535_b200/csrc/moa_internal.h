@@ -112,6 +112,12 @@ cudaError_t launch_radix2_stage(const double2 *in, double2 *out, int t, int q,
                                 int conj_out, cudaStream_t s);
 cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, int P,
                             int conj_out, cudaStream_t s);
+// one chunk g of the chunked exchange: recv holds [src][count] (stride count); column
+// c_local of the chunk is global column (inner_len)*(goff + (o % wg) + f1*(o / wg)) + i,
+// o = c_local / inner_len, i = c_local % inner_len; out[c + out_stride*k2]
+cudaError_t launch_pcombine_chunk(const double2 *recv, double2 *out, int64_t count, int P, int64_t inner_len,
+                                  int64_t wg, int64_t f1, int64_t goff, int64_t out_stride, int conj_out,
+                                  cudaStream_t s);
 cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int64_t count,
                                double2 *out, cudaStream_t s);
 

@@ -398,6 +398,36 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
     return MOA_OK;
 }
 
+// SURVEY §8(e) chunked exchange: the last pass of a 3-level p > 1 lifting split into G
+// groups of its middle digit w (k_1).  Group g writes its outputs, for every
+// destination, into send chunk g in the layout [g][dst][o][i] with
+// o = w_local + (F1/G)*k and i = T*u + t, so the all-to-all of chunk g can start while
+// group g+1 is being computed; pcombine_chunk maps the received chunk back to columns.
+int build_chunked_last(const moa_fft_plan_s *pl, const PassPlan &last, int G, std::vector<PassPlan> &out) {
+    out.clear();
+    const int64_t F0 = pl->lift[0], F1 = pl->lift[1], M = pl->M, P = pl->p;
+    if (pl->d != 3 || G < 2 || F1 % G) return fail(MOA_ERR_INVALID_ARG, "chunks=%d needs a 3-level lifting with G | F1", G);
+    const int64_t Wg = F1 / G;
+    for (int g = 0; g < G; ++g) {
+        PassPlan pp = last;
+        PassDesc &D = pp.d;
+        D.pack_lp = -1;
+        D.in_shift = -(int64_t)g * Wg * D.in_w;                   // w = g*Wg + w_local
+        D.a_c = (int64_t)((uint64_t)D.a_c + (uint64_t)D.a_w * (uint64_t)(g * Wg));
+        D.out_shift = -(int64_t)g * (M / G);                      // chunk g of the send buffer
+        D.out_v = M / (G * P);                                    // destination block inside the chunk
+        D.out_u = pp.T;
+        D.out_t = 1;
+        D.out_w = F0 / P;
+        D.out_k = Wg * (F0 / P);
+        pp.tiles = D.U * D.V * Wg;
+        pp.tma = 0;
+        pp.pf_grid = 0;
+        out.push_back(pp);
+    }
+    return MOA_OK;
+}
+
 void free_plan(moa_fft_plan_s *pl) {
     if (!pl) return;
     if (pl->rows) {
@@ -429,6 +459,13 @@ void free_plan(moa_fft_plan_s *pl) {
     cudaFree(pl->items);
     cudaFree(pl->counters);
     cudaFree(pl->scratch);
+    if (pl->comm_stream) cudaStreamDestroy(pl->comm_stream);
+    if (pl->comb_stream) cudaStreamDestroy(pl->comb_stream);
+    for (cudaEvent_t e : pl->ev_pass)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : pl->ev_a2a)
+        if (e) cudaEventDestroy(e);
+    if (pl->ev_comb) cudaEventDestroy(pl->ev_comb);
     if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
     if (pl->graph_stream) cudaStreamDestroy(pl->graph_stream);
     for (auto &r : pl->recs) {
@@ -673,6 +710,52 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         if (p == 1 && pl->d == 3 && fuse && (rc = setup_fused(pl, fuse)) != MOA_OK) {
             free_plan(pl);
             return rc;
+        }
+    }
+    // chunked NCCL exchange: G groups of the last pass's middle digit,
+    // each all-to-all overlapping the next group's butterflies.  Default G: per-peer
+    // chunks of >= 1 MiB, at most 8 (real ranks); EMULATED plans chunk only when asked.
+    if (opt && opt->chunks > 1 && !(p > 1 && exchange == MOA_XCHG_NCCL && pl->d == 3)) {
+        free_plan(pl);
+        return fail(MOA_ERR_INVALID_ARG, "chunks=%d needs p > 1, the NCCL exchange and a 3-level lifting", opt->chunks);
+    }
+    if (p > 1 && exchange == MOA_XCHG_NCCL && mode != MOA_MODE_LITERAL && pl->d == 3) {
+        int G = opt && opt->chunks > 0 ? opt->chunks : 0;
+        if (G == 0 && mode == MOA_MODE_LIFTED) {
+            G = 1;
+            while (G < 8 && (pl->M / (2 * G * p)) * 16 >= ((int64_t)1 << 20) && pl->lift[1] % (2 * G) == 0) G *= 2;
+        }
+        if (G > 1) {
+            if (!pow2(G) || pl->lift[1] % G) {
+                free_plan(pl);
+                return fail(MOA_ERR_INVALID_ARG, "chunks=%d must be a power of two dividing F1=%lld", G,
+                            (long long)pl->lift[1]);
+            }
+            if (mode == MOA_MODE_EMULATED) {
+                pl->rank_chunk_last.resize(p);
+                for (int r = 0; r < p; ++r)
+                    if ((rc = build_chunked_last(pl, pl->rank_passes[r].back(), G, pl->rank_chunk_last[r])) != MOA_OK) {
+                        free_plan(pl);
+                        return rc;
+                    }
+            } else if ((rc = build_chunked_last(pl, pl->passes.back(), G, pl->chunk_last)) != MOA_OK) {
+                free_plan(pl);
+                return rc;
+            }
+            pl->ev_pass.resize(G);
+            pl->ev_a2a.resize(G);
+            bool ok = cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking) == cudaSuccess &&
+                      cudaStreamCreateWithFlags(&pl->comb_stream, cudaStreamNonBlocking) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&pl->ev_comb, cudaEventDisableTiming) == cudaSuccess;
+            for (int g = 0; ok && g < G; ++g)
+                ok = cudaEventCreateWithFlags(&pl->ev_pass[g], cudaEventDisableTiming) == cudaSuccess &&
+                     cudaEventCreateWithFlags(&pl->ev_a2a[g], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) {
+                cudaGetLastError();
+                free_plan(pl);
+                return fail(MOA_ERR_CUDA, "chunk streams/events creation failed");
+            }
+            pl->chunks = G;
         }
     }
     // graph replay: single-GPU lifted plans whose launches do not change between

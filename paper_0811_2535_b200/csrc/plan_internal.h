@@ -75,6 +75,13 @@ struct moa_fft_plan_s {
     int d = 0;
     int64_t lift[4] = {0, 0, 0, 0};
     int chunks = 1;
+    // chunked NCCL exchange (p > 1, 3-level liftings): the last pass split into G groups
+    // of the middle digit; per group: pass -> all-to-all (comm stream) -> combine (side stream)
+    std::vector<moa::PassPlan> chunk_last;                   // real ranks: G group passes
+    std::vector<std::vector<moa::PassPlan>> rank_chunk_last; // emulated: per virtual rank
+    cudaStream_t comm_stream = nullptr, comb_stream = nullptr;
+    std::vector<cudaEvent_t> ev_pass, ev_a2a;
+    cudaEvent_t ev_comb = nullptr;
     int exchange = MOA_XCHG_NCCL;
     // P2P exchange: receive buffers of every rank (own = recv), double-buffered per execute
     double2 *peer_recv[16] = {};
@@ -137,6 +144,7 @@ namespace moa {
 int default_lifting(int tl, int64_t *lift, int p);
 int choose_T(int logF, int64_t avail);
 int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan> &out);
+int build_chunked_last(const moa_fft_plan_s *pl, const PassPlan &last, int G, std::vector<PassPlan> &out);
 void free_plan(moa_fft_plan_s *pl);
 int setup_fused(moa_fft_plan_s *pl, int kind);
 int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt);

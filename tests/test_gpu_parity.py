@@ -343,6 +343,29 @@ def test_emulated_fused_exchange(t, P):
     assert max(oracle.rel_l2(got[r], ref[r::P]) for r in range(P)) <= tol(t)
 
 
+@pytest.mark.parametrize("t,P,lift", [(20, 4, [16, 128, 128]), (23, 2, None), (24, 8, None), (24, 4, None)])
+def test_emulated_chunked_exchange_bitwise(t, P, lift):
+    """the exchange in G chunks of the last pass's middle digit gives the
+    same output bit for bit for every G, and X[r + P i] on rank r."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    outs = {}
+    for G in (1, 2, 4, 8):
+        plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, chunks=G, lift=lift)
+        assert plan.info()["chunks"] == G
+        outs[G] = _run(plan, xin)
+    for G in (2, 4, 8):
+        assert np.array_equal(outs[G], outs[1]), G
+    ref = oracle.fft(x, -1, threads=8)
+    got = outs[4].reshape(P, n // P)
+    assert max(oracle.rel_l2(got[r], ref[r::P]) for r in range(P)) <= tol(t)
+    with pytest.raises(moa.MoaError):
+        moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, chunks=3, lift=lift)
+    with pytest.raises(moa.MoaError):   # two-level lifting: nothing to chunk
+        moa.Plan(1 << 16, 2, -1, mode=moa.MODE_EMULATED, chunks=2)
+
+
 def test_emulated_with_lifting_depth3():
     t, P = 21, 4
     x = moa_inputs.signal_for(t)
