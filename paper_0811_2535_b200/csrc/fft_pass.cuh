@@ -110,7 +110,7 @@ __device__ __forceinline__ Tp *elem_off_c(Tp *p, uint32_t c, uint32_t stride) {
 // measured slower: more loads on the latency-critical path between the stages.)
 template <int RS>
 __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restrict__ tf, int e1) {
-    if (RS == 1 || e1 == 0) return;
+    if (RS == 1) return;   // (no e1 == 0 shortcut: a divergent exit costs more register moves than it saves)
     double2 w1 = __ldg(tf + e1);
     double2 w2 = RS > 2 ? __ldg(tf + 2 * e1) : w1;
     double2 w4 = RS > 4 ? __ldg(tf + 4 * e1) : w1;
