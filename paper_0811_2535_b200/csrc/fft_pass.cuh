@@ -324,7 +324,9 @@ __device__ __forceinline__ void rdb_load_tile(double2 *x, const PassDesc &d, con
 // per-point constants: global addresses are base + r*(NB*stride); shared
 // addresses use phys(j + r*NB) = (j ^ swz(j) ^ swz(r*NB)) + r*NB (the XOR fold is
 // linear over the disjoint bit fields of j and r*NB).
-template <int F, int T, int NS, bool FIRST, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
+// TW: 0 = the pass has no twiddle, 1 = it has one (both compile-time: no uniform branch
+// whose two register assignments the compiler must reconcile), 2 = d.twiddle at run time
+template <int F, int T, int NS, bool FIRST, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0, int TW = 2>
 __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
                                           const double2 *inbuf, const Hook &hook) {
     using SH = PassShape<F, T>;
@@ -375,7 +377,8 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
-        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        if (TW == 1 || (TW == 2 && d.twiddle))
+            build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         if constexpr (LAST) __syncthreads();   // single-stage transform: publish the tables
     } else if constexpr (FIRST && SRC == 6) {
         // register double buffering (fft_pass_rdb_kernel): this tile's points were loaded
@@ -387,7 +390,8 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
-        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        if (TW == 1 || (TW == 2 && d.twiddle))
+            build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
     } else if constexpr (FIRST && SRC == 3) {
         // prefetched by this same thread (cp.async, fft_pass_pf_kernel) into the
         // exchange layout: its own copies are visible after cp.async.wait_all
@@ -399,7 +403,8 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
-        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        if (TW == 1 || (TW == 2 && d.twiddle))
+            build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
     } else if constexpr (FIRST) {
 #pragma unroll
         for (int i = 0; i < M; ++i)
@@ -409,7 +414,8 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
             for (int k = 0; k < R; ++k) x[k].y = -x[k].y;
         }
-        if (d.twiddle) build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
+        if (TW == 1 || (TW == 2 && d.twiddle))
+            build_twiddle_tables<F, T>(d, const_cast<double2 *>(c.twa), const_cast<double2 *>(c.twb), c.al, c.be);
         if constexpr (SRC <= 2) hook();
     } else {
 #pragma unroll
@@ -461,7 +467,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         for (int i = 0; i < M; ++i) {
             const int t = tt[i], j = jj[i];
             double2 *v = x + i * RS;
-            if (d.twiddle) {
+            if (TW == 1 || (TW == 2 && d.twiddle)) {
                 const double2 a = c.twa[t * (NB + 1) + j];
                 v[0] = cmul(v[0], a);
 #pragma unroll
@@ -489,16 +495,16 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
     }
 }
 
-template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
+template <int F, int T, int NS, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0, int TW = 2>
 __device__ __forceinline__ void fft_stages(double2 *x, double2 *sm, const PassDesc &d, const TileCtx &c,
                                            const double2 *inbuf, const Hook &hook) {
     constexpr int RS = stage_radix(F, NS);
-    fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
-    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
+    fft_stage<F, T, NS, NS == 1, SRC, Hook, LD, ST, TW>(x, sm, d, c, inbuf, hook);
+    if constexpr (NS * RS < F) fft_stages<F, T, NS * RS, SRC, Hook, LD, ST, TW>(x, sm, d, c, inbuf, hook);
 }
 
 // one tile of T transforms; tile id -> (u, v, w) as documented in PassDesc
-template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0>
+template <int F, int T, int SRC = 0, class Hook = NoHook, int LD = 0, int ST = 0, int TW = 2>
 __device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDesc &d, const TileIO &io, int64_t b,
                                          const double2 *inbuf = nullptr, const Hook &hook = Hook()) {
     // batch index above the per-transform tile bits
@@ -525,10 +531,10 @@ __device__ __forceinline__ void tile_fft(double2 *sm, double2 *tw, const PassDes
     c.twa = twa;
     c.twb = twb;
     double2 x[PassShape<F, T>::R];
-    fft_stages<F, T, 1, SRC, Hook, LD, ST>(x, sm, d, c, inbuf, hook);
+    fft_stages<F, T, 1, SRC, Hook, LD, ST, TW>(x, sm, d, c, inbuf, hook);
 }
 
-template <int F, int T>
+template <int F, int T, int TW>
 __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     fft_pass_kernel(const PassDesc d) {
     extern __shared__ double2 sm[];
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
-    tile_fft<F, T>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
+    tile_fft<F, T, 0, NoHook, 0, 0, TW>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
                    blockIdx.x);
 }
 
@@ -720,6 +726,7 @@ int grid_one_pf() {
 template <int F, int T>
 cudaError_t launch_one(const PassDesc &d, int64_t tiles, cudaStream_t s) {
     using SH = PassShape<F, T>;
+    auto kernel = d.twiddle ? fft_pass_kernel<F, T, 1> : fft_pass_kernel<F, T, 0>;
     if (d.pdl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)tiles);
@@ -731,18 +738,22 @@ cudaError_t launch_one(const PassDesc &d, int64_t tiles, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, fft_pass_kernel<F, T>, d);
+        return cudaLaunchKernelEx(&cfg, kernel, d);
     }
-    fft_pass_kernel<F, T><<<(unsigned)tiles, SH::NT, SH::SMEM, s>>>(d);
+    kernel<<<(unsigned)tiles, SH::NT, SH::SMEM, s>>>(d);
     return cudaGetLastError();
 }
 
 template <int F, int T>
 cudaError_t prepare_one() {
     using SH = PassShape<F, T>;
-    if (SH::SMEM > 48 * 1024)
-        return cudaFuncSetAttribute(fft_pass_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (SH::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fft_pass_kernel<F, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)SH::SMEM);
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(fft_pass_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SH::SMEM);
+    }
     return cudaSuccess;
 }
 
