@@ -241,11 +241,11 @@ __global__ void __launch_bounds__(TicketShape<F2, T2, F3, T3>::NT, TicketShape<F
     const int64_t shift = (int64_t)g * fd.rows_per_group_elems;
     if (kind == 0) {
         TileIO io{fd.work, slot_ptr, 0, shift};
-        tile_fft<F2, T2, 0, NoHook, 2, 0>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH2),
+        tile_fft<F2, T2, 0, NoHook, 2, 0, 1>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH2),
                                           fd.p2, io, (int64_t)g * fd.tiles2 + tile);
     } else {
         TileIO io{slot_ptr, fd.out, shift, 0};
-        tile_fft<F3, T3, 0, NoHook, 1, 1>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH3),
+        tile_fft<F3, T3, 0, NoHook, 1, 1, 0>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + SH::XCH3),
                                           fd.p3, io, (int64_t)g + (int64_t)fd.groups * tile);
         if (fd.discard) {
             __syncthreads();   // every lane has loaded its scratch points
