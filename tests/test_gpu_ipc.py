@@ -1,13 +1,13 @@
 """The fused P2P exchange across a real process boundary (GPU box, one B200).
 
-Two processes (world size 2, gloo rendezvous on 127.0.0.1) each own a
+Two or four processes (gloo rendezvous on 127.0.0.1) each own a
 MOA_XCHG_P2P_EXTERNAL plan on cuda:0.  They swap the CUDA-IPC handles of their
 receive buffers through torch.distributed, so each process's last butterfly
-pass stores half of its output straight into the OTHER process's buffer (the
+pass stores (p-1)/p of its output straight into the OTHER processes' buffers (the
 Fig 5.9 redistribution, fused into the kernel).  Between phase 1
 and phase 2 the ranks meet at a host barrier (stream synchronise + gloo), so no
 kernel ever waits on another process's kernel.  Each rank must end with
-X[r + 2 i] of the oracle (xcyclic), over several executes (the
+X[r + p i] of the oracle (xcyclic), over several executes (the
 double-buffered receive halves alternate).
 """
 import os
@@ -68,20 +68,20 @@ def _worker(rank, world, port, t, q):
         q.put((rank, repr(e)))
 
 
-@pytest.mark.parametrize("t", [12, 20])
-def test_p2p_exchange_two_processes_one_gpu(t):
+@pytest.mark.parametrize("t,world", [(12, 2), (20, 2), (21, 4), (24, 4)])
+def test_p2p_exchange_processes_one_gpu(t, world):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, t, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, t, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    for r in range(2):
+    for r in range(world):
         assert not isinstance(res[r], str), res[r]
         assert res[r] <= 1e-12 * t, (r, res[r])
