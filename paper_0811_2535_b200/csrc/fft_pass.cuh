@@ -108,6 +108,41 @@ __device__ __forceinline__ Tp *elem_off_c(Tp *p, uint32_t c, uint32_t stride) {
 // stage twiddles omega_{Ns*RS}^(r*k) = omega_FMAX^(r*e1), e1 = k*FMAX/(Ns*RS): 4 table
 // loads (r = 1, 2, 4, 8) and products for the rest.  (One table load per point was
 // measured slower: more loads on the latency-critical path between the stages.)
+// stage_twiddle with the pass twiddle's butterfly-constant factor a = omega^(al+be*j)
+// folded in (last stage of a twiddled pass): x[s] *= a * omega_F^(j*s).  DFT linearity
+// moves a from the 16 outputs to the 16 inputs, where it rides on the stage twiddles'
+// power chain (c_s = c_lo * w_hi): 16 + 4 products instead of 15 + 16.
+template <int RS>
+__device__ __forceinline__ void stage_twiddle_scaled(double2 *x, const double2 *__restrict__ tf, int e1, double2 a) {
+    x[0] = cmul(x[0], a);
+    if (RS == 1) return;
+    double2 w1 = __ldg(tf + e1);
+    double2 w2 = RS > 2 ? __ldg(tf + 2 * e1) : w1;
+    double2 w4 = RS > 4 ? __ldg(tf + 4 * e1) : w1;
+    double2 w8 = RS > 8 ? __ldg(tf + 8 * e1) : w1;
+    double2 c1 = cmul(a, w1);
+    x[1] = cmul(x[1], c1);
+    if (RS == 2) return;
+    double2 c2 = cmul(a, w2), c3 = cmul(c1, w2);
+    x[2] = cmul(x[2], c2);
+    x[3] = cmul(x[3], c3);
+    if (RS == 4) return;
+    double2 c4 = cmul(a, w4), c5 = cmul(c1, w4), c6 = cmul(c2, w4), c7 = cmul(c3, w4);
+    x[4] = cmul(x[4], c4);
+    x[5] = cmul(x[5], c5);
+    x[6] = cmul(x[6], c6);
+    x[7] = cmul(x[7], c7);
+    if (RS == 8) return;
+    x[8] = cmul(x[8], cmul(a, w8));
+    x[9] = cmul(x[9], cmul(c1, w8));
+    x[10] = cmul(x[10], cmul(c2, w8));
+    x[11] = cmul(x[11], cmul(c3, w8));
+    x[12] = cmul(x[12], cmul(c4, w8));
+    x[13] = cmul(x[13], cmul(c5, w8));
+    x[14] = cmul(x[14], cmul(c6, w8));
+    x[15] = cmul(x[15], cmul(c7, w8));
+}
+
 template <int RS>
 __device__ __forceinline__ void stage_twiddle(double2 *x, const double2 *__restrict__ tf, int e1) {
     if (RS == 1) return;   // (no e1 == 0 shortcut: a divergent exit costs more register moves than it saves)
@@ -434,10 +469,16 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         // kernel starts the next tile's copy into it here (hook = barrier + cp.async)
         if constexpr (LAST && SRC >= 3) hook();
     }
-    // ---- twiddle + radix-RS butterflies in registers
+    // ---- twiddle + radix-RS butterflies in registers (FOLD: the last stage of a
+    //      twiddled pass takes the pass twiddle's factor A[t][j] on its inputs)
+    constexpr bool FOLD = LAST && NS > 1 && TW == 1;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-        if (NS > 1) stage_twiddle<RS>(x + i * RS, d.tw_f, (jj[i] % NS) * (FMAX / (NS * RS)));
+        if constexpr (FOLD)
+            stage_twiddle_scaled<RS>(x + i * RS, d.tw_f, (jj[i] % NS) * (FMAX / (NS * RS)),
+                                     c.twa[tt[i] * (NB + 1) + jj[i]]);
+        else if (NS > 1)
+            stage_twiddle<RS>(x + i * RS, d.tw_f, (jj[i] % NS) * (FMAX / (NS * RS)));
         dft_reg<RS>(x + i * RS);
     }
     if constexpr (!LAST) {
@@ -467,7 +508,10 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         for (int i = 0; i < M; ++i) {
             const int t = tt[i], j = jj[i];
             double2 *v = x + i * RS;
-            if (TW == 1 || (TW == 2 && d.twiddle)) {
+            if constexpr (FOLD) {   // output r: times B[t][r] (B[t][0] = 1)
+#pragma unroll
+                for (int r = 1; r < RS; ++r) v[r] = cmul(v[r], c.twb[t * (RS + 1) + r]);
+            } else if (TW == 1 || (TW == 2 && d.twiddle)) {
                 const double2 a = c.twa[t * (NB + 1) + j];
                 v[0] = cmul(v[0], a);
 #pragma unroll
