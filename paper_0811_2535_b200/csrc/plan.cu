@@ -167,6 +167,12 @@ int default_lifting(int tl, int64_t *lift, int p) {
         lift[1] = (int64_t)1 << (tl - a);
         return 2;
     }
+    if (tl == 21 || tl == 22) {   // <128, 256, 2^(tl-15)>: 2^21 38.9 vs 47.1 us as <32,256,256>,
+        lift[0] = 128;               // 2^22 69.7 vs 73.8 us as <64,256,256> (tools/tune_probe.py):
+        lift[1] = 256;               // a <= 64-point first pass (T >= 32) is the slowest of the three
+        lift[2] = (int64_t)1 << (tl - 15);
+        return 3;
+    }
     if (tl >= 25 && tl <= 28) {   // <256, 256, 2^(tl-16)>: the long factor in the row pass
         lift[0] = 256;
         lift[1] = 256;

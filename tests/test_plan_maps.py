@@ -117,6 +117,9 @@ def test_default_lifting_table_every_t_and_p():
                 assert lift[0] >= p, (t, p, lift)
     assert moa.default_lifting(1 << 24) == [256, 256, 256]
     assert moa.default_lifting(1 << 20) == [1024, 1024]
+    assert moa.default_lifting(1 << 21) == [128, 256, 64]
+    assert moa.default_lifting(1 << 22) == [128, 256, 128]
+    assert moa.default_lifting(1 << 23) == [128, 256, 256]
     assert moa.default_lifting(1 << 26) == [256, 256, 1024]
     assert moa.default_lifting(1 << 30) == [128, 128, 256, 256]
     assert moa.default_lifting(1 << 10) == [1024]

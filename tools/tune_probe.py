@@ -1,0 +1,56 @@
+"""Lifting / tile-size tuning probe for the mid sizes (development tool, not the bench).
+
+For every t, every candidate lifting and every (MOA_FFT_MINTILES, MOA_FFT_TF) setting:
+median of REPS L2-flushed executes (tools/perf_probe.time_plan).  The env knobs are read at
+plan creation, so they are set in-process between plans.
+
+    python tools/tune_probe.py 17 23 > gpurun_out/tune.jsonl
+"""
+import itertools
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import perf_probe  # noqa: E402
+
+
+def liftings(t):
+    out = []
+    for a in range(max(1, t - 13), min(13, t - 1) + 1):
+        out.append([1 << a, 1 << (t - a)])
+    for a in range(3, 9):
+        for b in range(5, 11):
+            c = t - a - b
+            if 5 <= c <= 12:
+                out.append([1 << a, 1 << b, 1 << c])
+    return out
+
+
+def main():
+    t0, t1 = int(sys.argv[1]), int(sys.argv[2])
+    for t in range(t0, t1 + 1):
+        best = None
+        for lift in liftings(t):
+            for mt, tf in itertools.product((128, 296, 592), (2048, 4096, 8192)):
+                os.environ["MOA_FFT_MINTILES"] = str(mt)
+                os.environ["MOA_FFT_TF"] = str(tf)
+                try:
+                    r = perf_probe.time_plan(t, lift, reps=10)
+                except Exception as e:   # unsupported (F, T) combination
+                    print(json.dumps({"t": t, "lift": lift, "mintiles": mt, "tf": tf, "error": str(e)[:80]}))
+                    continue
+                r["mintiles"] = mt
+                print(json.dumps(r), flush=True)
+                if best is None or r["us"] < best["us"]:
+                    best = r
+        os.environ.pop("MOA_FFT_MINTILES", None)
+        os.environ.pop("MOA_FFT_TF", None)
+        d = perf_probe.time_plan(t, None, reps=10)
+        print(json.dumps({"t": t, "default": d["lift"], "default_us": d["us"], "best": best["lift"],
+                          "best_us": best["us"], "best_mintiles": best["mintiles"], "best_tf": best["tf"]}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
