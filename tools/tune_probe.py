@@ -5,6 +5,7 @@ median of REPS L2-flushed executes (tools/perf_probe.time_plan).  The env knobs 
 plan creation, so they are set in-process between plans.
 
     python tools/tune_probe.py 17 23 > gpurun_out/tune.jsonl
+    python tools/tune_probe.py 25 28 big > gpurun_out/tune_big.jsonl
 """
 import itertools
 import json
@@ -27,16 +28,35 @@ def liftings(t):
     return out
 
 
+def liftings_big(t):
+    """3-level liftings with factors in [2^5, 2^12] and 4-level ones in [2^4, 2^10]."""
+    out = []
+    for a in range(5, 13):
+        for b in range(5, 13):
+            c = t - a - b
+            if 5 <= c <= 12:
+                out.append([1 << a, 1 << b, 1 << c])
+    for a in range(4, 11):
+        for b in range(4, 11):
+            for c in range(4, 11):
+                e = t - a - b - c
+                if 4 <= e <= 10:
+                    out.append([1 << a, 1 << b, 1 << c, 1 << e])
+    return out
+
+
 def main():
     t0, t1 = int(sys.argv[1]), int(sys.argv[2])
+    big = len(sys.argv) > 3 and sys.argv[3] == "big"   # default knobs, 3 reps, 3/4-level liftings
     for t in range(t0, t1 + 1):
         best = None
-        for lift in liftings(t):
-            for mt, tf in itertools.product((128, 296, 592), (2048, 4096, 8192)):
-                os.environ["MOA_FFT_MINTILES"] = str(mt)
-                os.environ["MOA_FFT_TF"] = str(tf)
+        for lift in (liftings_big(t) if big else liftings(t)):
+            for mt, tf in (((128, 8192),) if big else itertools.product((128, 296, 592), (2048, 4096, 8192))):
+                if not big:   # big: the plan's own T rules
+                    os.environ["MOA_FFT_MINTILES"] = str(mt)
+                    os.environ["MOA_FFT_TF"] = str(tf)
                 try:
-                    r = perf_probe.time_plan(t, lift, reps=10)
+                    r = perf_probe.time_plan(t, lift, reps=3 if big else 10)
                 except Exception as e:   # unsupported (F, T) combination
                     print(json.dumps({"t": t, "lift": lift, "mintiles": mt, "tf": tf, "error": str(e)[:80]}))
                     continue
