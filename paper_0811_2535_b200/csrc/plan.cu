@@ -260,8 +260,9 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
             // every (a, b); twiddle omega_{F*B}^(b*k) = omega_n^(b*k*n/(F*B)); in place.
             int T = fill_T(choose_T(pp.logF, B), pl->M / F, pl->batch);
             // first column pass over rows >= 1 MiB apart: 256-byte runs (T*F = 4096, 2 tiles
-            // per SM) -- each 128-byte run of a T = 8 tile opens its own DRAM page
-            if (i == 0 && pp.logF <= 8 && (int64_t)16 * B >= env_int("MOA_FFT_WIDE", 1 << 20) &&
+            // per SM) -- each 128-byte run of a T = 8 tile opens its own DRAM page (F = 256
+            // only: 64- and 128-point first passes of 2^29 / 2^30 lose 2-3 % at T = 64 / 32)
+            if (i == 0 && pp.logF == 8 && (int64_t)16 * B >= env_int("MOA_FFT_WIDE", 1 << 20) &&
                 T == (2048 >> pp.logF) && 2 * T <= B && pass_supported(pp.logF, 2 * T) && pl->batch == 1)
                 T *= 2;
             pp.T = T;
