@@ -84,6 +84,21 @@ typedef struct {
                             transforms stored back to back (transform b at elements
                             [b*n, (b+1)*n) of in and out); 0 or 1 = one transform.
                             Every pass covers the whole batch in one launch.           */
+    int breakpoint;      /* p > 1: the stage q at which Fig 5.7's cyclic phase starts
+                            (the paper's breakpoint, range [log2 m + 1, log2 psize + 1],
+                            P:665).  0 or log2(psize)+1 = the high end: phase 1
+                            = the full local psize-point FFT, phase 2 = one m-point DFT
+                            (pcombine).  log2(m)+1 = the low end: phase 1 = the
+                            m-point DFTs of stages 1..log2 m at local stride psize/m
+                            with the weightcyclic factor omega_n^((r+m*c)*u) fused
+                            (psplit kernel), then the exchange, then the m FFTs of
+                            length psize/m of the received [source][c] blocks (one
+                            batched plan; lift[] is ITS lifting, product n/m^2) and an
+                            m-point DFT with the factor omega_psize^(s*c) on its loads
+                            (pcombine).  Both ends leave X[r + m*i] at out[i] on rank
+                            r.  Other values: MOA_ERR_INVALID_ARG (the oracle's Fig 5.7
+                            simulation covers every breakpoint).  The low end needs the
+                            NCCL exchange (or EMULATED) and psize >= 2m.               */
 } moa_fft_options;
 
 typedef struct {
@@ -96,7 +111,8 @@ typedef struct {
     int64_t local_n;     /* elements per rank: n / p (the paper's psize)               */
     int passes;          /* kernel passes over the local data (lifting depth d)       */
     int64_t lift[4];     /* lifting factors <F1..Fd>                                  */
-    int breakpoint;      /* q at which the cyclic phase starts: log2(psize)+1  */
+    int breakpoint;      /* q at which the cyclic phase starts: log2(psize)+1 (P:289,
+                            default) or log2(m)+1 (options.breakpoint)         */
     int chunks;          /* all-to-all chunks G                                       */
     int launches;        /* kernels one execute launches (not counting NCCL's)        */
     int64_t workspace_bytes;  /* device bytes the plan owns                            */

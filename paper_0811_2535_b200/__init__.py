@@ -36,7 +36,7 @@ class MoaError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("nlift", ctypes.c_int), ("lift", ctypes.c_int64 * 4),
                 ("chunks", ctypes.c_int), ("exchange", ctypes.c_int), ("rank", ctypes.c_int),
-                ("batch", ctypes.c_int64)]
+                ("batch", ctypes.c_int64), ("breakpoint", ctypes.c_int)]
 
 
 class _KernelStat(ctypes.Structure):
@@ -129,14 +129,17 @@ class Plan:
     n, p, sign: see include/moa_fft.h.  mode: MODE_LIFTED (product path),
     MODE_LITERAL (paper-literal bitrev + t radix-2 stages, ablation),
     MODE_EMULATED (p virtual ranks on one GPU).  lift: optional lifting <F1..Fd>.
+    breakpoint (p > 1): 0 = the high end log2(n/p)+1, or log2(p)+1 = the low end
+    (Fig 5.7's cyclic phase starts after the first log2 p stages; include/moa_fft.h).
     """
 
     def __init__(self, n: int, p: int = 1, sign: int = -1, mode: int = MODE_LIFTED,
                  lift=None, chunks: int = 0, stream=None, exchange: int = XCHG_NCCL, rank: int = 0,
-                 batch: int = 1):
+                 batch: int = 1, breakpoint: int = 0):
         lib = load()
         opt = _Options()
         opt.mode = mode
+        opt.breakpoint = breakpoint
         opt.chunks = chunks
         opt.exchange = exchange
         opt.rank = rank
@@ -369,13 +372,14 @@ def gen_uniform(seed: int, count: int, out, first: int = 0, stride: int = 1, str
     return out
 
 
-def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
+def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None, breakpoint: int = 0):
     """Host-only index maps of one lifted pass (moa_fft_describe_pass; no GPU needed).
 
     Returns (F, in_idx, out_idx, tw_exp) as numpy int64 arrays of n/p entries."""
     import numpy as np
     lib = load()
     opt = _Options()
+    opt.breakpoint = breakpoint
     if lift:
         opt.nlift = len(lift)
         for i, f in enumerate(lift):
@@ -390,15 +394,16 @@ def describe_pass(n: int, p: int, rank: int, pass_index: int, lift=None):
     return int(F.value), a, b, c
 
 
-def dist_fft(x_local, n: int, sign: int = -1, out=None, exchange: int = XCHG_NCCL):
+def dist_fft(x_local, n: int, sign: int = -1, out=None, exchange: int = XCHG_NCCL, breakpoint: int = 0):
     """One partitioned n-point transform over the torch.distributed world (after dist_init):
     x_local = x[rank::p] (complex128, this rank's GPU) -> X[rank::p] (the paper's xcyclic,
     P:799).  Collective: every rank calls it.  exchange = XCHG_P2P fuses the
-    all-to-all into the last pass (the plan maps the peers' buffers first)."""
+    all-to-all into the last pass (the plan maps the peers' buffers first).  breakpoint:
+    see Plan (both ends give the same X[rank::p])."""
     import torch
     import torch.distributed as dist
     p = dist.get_world_size()
-    plan = Plan(n, p, sign, exchange=exchange)
+    plan = Plan(n, p, sign, exchange=exchange, breakpoint=breakpoint)
     try:
         if exchange == XCHG_P2P:
             plan.enable_p2p()

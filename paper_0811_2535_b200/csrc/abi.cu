@@ -254,7 +254,7 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
     o->local_n = pl->M;
     o->passes = pl->mode == MOA_MODE_LITERAL ? pl->t + 1 : pl->d;
     for (int i = 0; i < 4; ++i) o->lift[i] = pl->lift[i];
-    o->breakpoint = ilog2(pl->M) + 1;
+    o->breakpoint = pl->lowend ? ilog2(pl->p) + 1 : ilog2(pl->M) + 1;
     o->chunks = pl->chunks;
     if (pl->mode == MOA_MODE_LITERAL) {
         o->launches = pl->t + 1;
@@ -263,9 +263,9 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
         o->launches = pl->fused ? pl->d - 1 : pl->d;
         o->hbm_bytes = 32 * pl->n * pl->batch * (pl->fused ? pl->d - 1 : pl->d);
     } else {
-        int per_rank = pl->d + 1;
+        int per_rank = pl->lowend ? pl->d + 2 : pl->d + 1;   // (psplit +) passes + pcombine
         o->launches = pl->mode == MOA_MODE_EMULATED ? pl->p * per_rank : per_rank;
-        o->hbm_bytes = 32 * pl->M * (pl->d + 1) * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
+        o->hbm_bytes = 32 * pl->M * per_rank * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
         o->a2a_bytes = 16 * pl->M / pl->p * (pl->p - 1) * (pl->mode == MOA_MODE_EMULATED ? pl->p : 1);
     }
     o->workspace_bytes = pl->workspace_bytes;
@@ -299,8 +299,12 @@ int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opt
     tmp.p = p;
     tmp.M = n / p;
     tmp.hbits = (tmp.t + 1) / 2;
-    int rc = resolve_lifting(&tmp, opts);
+    int rc = resolve_breakpoint(&tmp, opts);
     if (rc) return rc;
+    if (tmp.lowend)
+        return fail(MOA_ERR_INVALID_ARG, "low-end breakpoint plans run a batched n/p^2-point plan between psplit "
+                                         "and pcombine: describe that plan (p = 1, batch = p)");
+    if ((rc = resolve_lifting(&tmp, opts)) != MOA_OK) return rc;
     std::vector<PassPlan> ps;
     if ((rc = build_passes(&tmp, rank, p, ps)) != MOA_OK) return rc;
     if (pass < 0 || pass >= (int)ps.size())
@@ -382,6 +386,21 @@ int moa_fft_get_profile(moa_fft_plan_t pl, moa_fft_kernel_stat *stats, int max_s
             memcpy(stats[i].name, tmp, sizeof tmp);
         }
         return k + k2;
+    }
+    if (pl->lowsub) {   // low-end breakpoint: the batched block FFTs ("blocks ..."), then psplit/pcombine
+        moa_fft_plan_s *sub = pl->lowsub;
+        sub->stream = pl->stream;
+        int k = moa_fft_get_profile(sub, stats, max_stats);
+        if (k < 0) return k;
+        for (int i = 0; stats && i < k; ++i) {
+            char tmp[64];
+            snprintf(tmp, sizeof tmp, "blocks %s", stats[i].name);
+            memcpy(stats[i].name, tmp, sizeof tmp);
+        }
+        pl->lowsub = nullptr;
+        int k2 = moa_fft_get_profile(pl, stats ? stats + k : nullptr, max_stats - k);
+        pl->lowsub = sub;
+        return k2 < 0 ? k2 : k + k2;
     }
     CUDA_TRY(cudaStreamSynchronize(pl->stream));
     for (auto &sl : pl->slots) {

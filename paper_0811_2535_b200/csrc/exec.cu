@@ -159,6 +159,42 @@ int execute(moa_fft_plan_s *pl, const double2 *in, double2 *out) {
 
     const int P = pl->p;
     const int64_t M = pl->M, chunk = M / P;
+    if (pl->lowend) {
+        // low-end breakpoint: psplit (stages 1..log2 P + weightcyclic) -> exchange -> the P
+        // (M/P)-point FFTs of the received blocks (lowsub) -> pcombine with omega_M^(r*v1)
+        const bool emu = pl->mode == MOA_MODE_EMULATED;
+        const int nr = emu ? P : 1;
+        for (int r = 0; r < nr; ++r) {
+            ProfScope sc(pl, "psplit", 32 * M);
+            CUDA_TRY(launch_psplit(in + r * M, pl->send + r * M, chunk, P, emu ? r : pl->rank, pl->n, pl->tw_hi,
+                                   pl->tw_lo, pl->hbits, pl->sign > 0, s));
+        }
+        if (emu) {
+            for (int dd = 0; dd < P; ++dd)
+                for (int sr = 0; sr < P; ++sr)
+                    CUDA_TRY(cudaMemcpyAsync(pl->recv + dd * M + sr * chunk, pl->send + sr * M + dd * chunk,
+                                             chunk * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        } else {
+            std::string err;
+            int rc;
+            {
+                ProfScope sc(pl, "alltoall (NCCL)", 16 * chunk * (P - 1));
+                rc = dist_alltoall(pl->send, pl->recv, chunk, P, pl->rank, s, &err);
+            }
+            if (rc) return fail(rc, "%s", err.c_str());
+        }
+        moa_fft_plan_s *sub = pl->lowsub;
+        sub->stream = s;
+        sub->profiling = pl->profiling;
+        for (int dd = 0; dd < nr; ++dd) {
+            int rc = execute(sub, pl->recv + dd * M, pl->work);
+            if (rc) return rc;
+            ProfScope sc(pl, "pcombine+tw", 32 * M);
+            CUDA_TRY(launch_pcombine_tw(pl->work, out + dd * M, chunk, P, pl->n, pl->tw_hi, pl->tw_lo, pl->hbits,
+                                        pl->sign > 0, s));
+        }
+        return MOA_OK;
+    }
     if (pl->mode == MOA_MODE_EMULATED && pl->exchange != MOA_XCHG_NCCL) {
         // fused exchange: virtual rank r's last pass stores straight into every
         // destination's receive block (recv + d*M + r*chunk)

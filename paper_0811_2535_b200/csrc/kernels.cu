@@ -257,6 +257,104 @@ cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, in
     return cudaGetLastError();
 }
 
+// K6' psplit<P>: the low-end breakpoint's phase 1 (Fig 5.7 with breakpoint = log2 m + 1,
+// P:665/694).  Rank r holds x[r + P*j'] (its block of P_n x); stages 1..log2 P
+// of Fig 3.9 on that block are the P-point DFTs over j' = c + chunk*s (stride psize/m),
+// and the weightcyclic factor of the following cyclic phase (Fig 4.4),
+// omega_n^((r + P*c)*u), is applied before the element leaves for rank u.
+template <int P>
+__global__ void __launch_bounds__(256) psplit_kernel(const double2 *__restrict__ in, double2 *__restrict__ send,
+                                                     int64_t chunk, uint64_t r, uint64_t nmask,
+                                                     const double2 *__restrict__ tw_hi,
+                                                     const double2 *__restrict__ tw_lo, int hbits, int conj_in) {
+    const uint64_t lomask = (1ull << hbits) - 1;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < chunk;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        double2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+            v[s] = __ldg(in + c + chunk * s);
+            if (conj_in) v[s].y = -v[s].y;
+        }
+        dft_reg<P>(v);
+        const uint64_t e1 = (r + (uint64_t)P * (uint64_t)c) & nmask;
+        __stcs(send + c, v[0]);
+#pragma unroll
+        for (int u = 1; u < P; ++u) {
+            const uint64_t e = (e1 * (uint64_t)u) & nmask;
+            const double2 w = cmul(__ldg(tw_hi + (e >> hbits)), __ldg(tw_lo + (e & lomask)));
+            __stcs(send + c + chunk * u, cmul(v[u], w));
+        }
+    }
+}
+
+cudaError_t launch_psplit(const double2 *in, double2 *send, int64_t chunk, int P, int64_t r, int64_t n,
+                          const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_in, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (chunk + 255) / 256;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    const uint64_t nm = (uint64_t)n - 1;
+    switch (P) {
+    case 2: psplit_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(in, send, chunk, r, nm, tw_hi, tw_lo, hbits, conj_in); break;
+    case 4: psplit_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(in, send, chunk, r, nm, tw_hi, tw_lo, hbits, conj_in); break;
+    case 8: psplit_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(in, send, chunk, r, nm, tw_hi, tw_lo, hbits, conj_in); break;
+    case 16: psplit_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(in, send, chunk, r, nm, tw_hi, tw_lo, hbits, conj_in); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// pcombine with the low-end breakpoint's inner twiddle: block s of recv is the
+// (M/P)-point FFT of source s's W[s][c]; column c is scaled by omega_M^(s*c) =
+// omega_n^(P*s*c) before the P-point DFT over s (exec.cu's lowend derivation).
+template <int P>
+__global__ void __launch_bounds__(256) pcombine_tw_kernel(const double2 *__restrict__ recv,
+                                                          double2 *__restrict__ out, int64_t chunk, uint64_t nmask,
+                                                          const double2 *__restrict__ tw_hi,
+                                                          const double2 *__restrict__ tw_lo, int hbits,
+                                                          int conj_out) {
+    const uint64_t lomask = (1ull << hbits) - 1;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < chunk;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        double2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) v[s] = __ldg(recv + s * chunk + c);
+        const uint64_t e1 = ((uint64_t)P * (uint64_t)c) & nmask;
+#pragma unroll
+        for (int s = 1; s < P; ++s) {
+            const uint64_t e = (e1 * (uint64_t)s) & nmask;
+            v[s] = cmul(v[s], cmul(__ldg(tw_hi + (e >> hbits)), __ldg(tw_lo + (e & lomask))));
+        }
+        dft_reg<P>(v);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double2 o = v[k];
+            if (conj_out) o.y = -o.y;
+            __stcs(out + c + chunk * k, o);
+        }
+    }
+}
+
+cudaError_t launch_pcombine_tw(const double2 *recv, double2 *out, int64_t chunk, int P, int64_t n,
+                               const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_out, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (chunk + 255) / 256;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    const uint64_t nm = (uint64_t)n - 1;
+    switch (P) {
+    case 2: pcombine_tw_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, nm, tw_hi, tw_lo, hbits, conj_out); break;
+    case 4: pcombine_tw_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, nm, tw_hi, tw_lo, hbits, conj_out); break;
+    case 8: pcombine_tw_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, nm, tw_hi, tw_lo, hbits, conj_out); break;
+    case 16: pcombine_tw_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(recv, out, chunk, nm, tw_hi, tw_lo, hbits, conj_out); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 // Chunked form (SURVEY §8(e) overlap): chunk g of the receive buffer, [src][count],
 // column c_local -> global column c = inner_len*(goff + (o % wg) + f1*(o / wg)) + i.
 template <int P>

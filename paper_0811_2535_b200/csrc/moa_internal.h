@@ -118,6 +118,14 @@ cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, in
 cudaError_t launch_pcombine_chunk(const double2 *recv, double2 *out, int64_t count, int P, int64_t inner_len,
                                   int64_t wg, int64_t f1, int64_t goff, int64_t out_stride, int conj_out,
                                   cudaStream_t s);
+// low-end breakpoint phase 1 (rank r): Z_c[u] = sum_s x[c + chunk*s] omega_P^(s*u),
+// times omega_n^((r + P*c)*u), stored at send[u*chunk + c]
+cudaError_t launch_psplit(const double2 *in, double2 *send, int64_t chunk, int P, int64_t r, int64_t n,
+                          const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_in, cudaStream_t s);
+// low-end breakpoint phase 3: v[s] = recv[s*chunk + c] * omega_n^(P*s*c), P-point DFT,
+// out[c + chunk*k]
+cudaError_t launch_pcombine_tw(const double2 *recv, double2 *out, int64_t chunk, int P, int64_t n,
+                               const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_out, cudaStream_t s);
 cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int64_t count,
                                double2 *out, cudaStream_t s);
 

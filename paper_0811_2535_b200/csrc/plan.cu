@@ -442,6 +442,10 @@ int build_chunked_last(const moa_fft_plan_s *pl, const PassPlan &last, int G, st
 
 void free_plan(moa_fft_plan_s *pl) {
     if (!pl) return;
+    if (pl->lowsub) {
+        free_plan(pl->lowsub);
+        pl->lowsub = nullptr;
+    }
     if (pl->rows) {
         free_plan(pl->rows);
         pl->rows = nullptr;
@@ -592,6 +596,23 @@ int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt) {
     return MOA_OK;
 }
 
+int resolve_breakpoint(moa_fft_plan_s *pl, const moa_fft_options *opt) {
+    const int bp = opt ? opt->breakpoint : 0;
+    const int lm = ilog2(pl->p), lps = ilog2(pl->M);
+    pl->lowend = false;
+    if (bp == 0 || bp == lps + 1) return MOA_OK;
+    if (pl->p > 1 && bp == lm + 1) {
+        if (pl->M < 2 * (int64_t)pl->p)
+            return fail(MOA_ERR_INVALID_ARG, "low-end breakpoint needs n/p >= 2p (psize = %lld, p = %d)",
+                        (long long)pl->M, pl->p);
+        pl->lowend = true;
+        return MOA_OK;
+    }
+    return fail(MOA_ERR_INVALID_ARG,
+                "breakpoint %d: the GPU path runs the high end %d (P:289) or, for p > 1, the low end %d (P:694)", bp,
+                lps + 1, lm + 1);
+}
+
 int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_plan_s **res) {
     *res = nullptr;
     int mode = opt ? opt->mode : MOA_MODE_LIFTED;
@@ -642,9 +663,37 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
     pl->exchange = exchange;
     pl->M = n / p;
     CUDA_TRY(cudaGetDevice(&pl->device));
-    if ((rc0 = resolve_lifting(pl, opt)) != MOA_OK) {
+    if ((rc0 = resolve_breakpoint(pl, opt)) != MOA_OK) {
         delete pl;
         return rc0;
+    }
+    if (pl->lowend) {
+        // low-end breakpoint (Fig 5.7, breakpoint = log2 m + 1).  Rank u receives
+        // W[j''] for j'' = r + P*c in [source r][c] blocks and needs X[u + P*v] =
+        // sum_j'' omega_M^(j''*v) W[j''].  With v = v1 + (M/P)*v2:
+        //   X = sum_r omega_P^(r*v2) * omega_M^(r*v1) * [sum_c omega_{M/P}^(c*v1) W[r][c]]
+        // -- P contiguous (M/P)-point FFTs (a batched p = 1 plan; options.lift is ITS
+        // lifting), then pcombine with the omega_M^(r*v1) factor on its loads.
+        moa_fft_options so = {};
+        so.mode = MOA_MODE_LIFTED;
+        so.batch = p;
+        if (opt && opt->nlift > 0) {
+            so.nlift = opt->nlift;
+            for (int i = 0; i < opt->nlift && i < 4; ++i) so.lift[i] = opt->lift[i];
+        }
+        if ((rc0 = make_plan(pl->M / p, 1, -1, &so, &pl->lowsub)) != MOA_OK) {
+            delete pl;
+            return rc0;
+        }
+        pl->d = pl->lowsub->d;
+        for (int i = 0; i < 4; ++i) pl->lift[i] = pl->lowsub->lift[i];
+    } else if ((rc0 = resolve_lifting(pl, opt)) != MOA_OK) {
+        delete pl;
+        return rc0;
+    }
+    if (pl->lowend && exchange != MOA_XCHG_NCCL) {
+        delete pl;
+        return fail(MOA_ERR_INVALID_ARG, "the low-end breakpoint runs with the NCCL exchange (or EMULATED ranks)");
     }
     pl->chunks = 1;
 
@@ -691,7 +740,7 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
     if (mode == MOA_MODE_LITERAL) {
         pl->work_elems = n;
     } else {
-        pl->work_elems = pl->d > 1 ? pl->M * pl->batch : 0;
+        pl->work_elems = (pl->d > 1 || pl->lowend) ? pl->M * pl->batch : 0;
         if (p > 1) pl->send_elems = (mode == MOA_MODE_EMULATED) ? n : pl->M;
     }
     // P2P: no send buffer; real ranks double-buffer the receive buffer (one barrier per execute)
@@ -702,7 +751,9 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         free_plan(pl);
         return rc;
     }
-    if (mode == MOA_MODE_EMULATED) {
+    if (pl->lowend) {
+        // no passes of its own: psplit, the exchange, lowsub, pcombine (exec.cu)
+    } else if (mode == MOA_MODE_EMULATED) {
         pl->rank_passes.resize(p);
         for (int r = 0; r < p; ++r)
             if ((rc = build_passes(pl, r, p, pl->rank_passes[r])) != MOA_OK) {
@@ -727,11 +778,11 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
     // chunked NCCL exchange: G groups of the last pass's middle digit,
     // each all-to-all overlapping the next group's butterflies.  Default G: per-peer
     // chunks of >= 1 MiB, at most 8 (real ranks); EMULATED plans chunk only when asked.
-    if (opt && opt->chunks > 1 && !(p > 1 && exchange == MOA_XCHG_NCCL && pl->d == 3)) {
+    if (opt && opt->chunks > 1 && !(p > 1 && exchange == MOA_XCHG_NCCL && pl->d == 3 && !pl->lowend)) {
         free_plan(pl);
         return fail(MOA_ERR_INVALID_ARG, "chunks=%d needs p > 1, the NCCL exchange and a 3-level lifting", opt->chunks);
     }
-    if (p > 1 && exchange == MOA_XCHG_NCCL && mode != MOA_MODE_LITERAL && pl->d == 3) {
+    if (p > 1 && exchange == MOA_XCHG_NCCL && mode != MOA_MODE_LITERAL && pl->d == 3 && !pl->lowend) {
         int G = opt && opt->chunks > 0 ? opt->chunks : 0;
         if (G == 0 && mode == MOA_MODE_LIFTED) {
             G = 1;

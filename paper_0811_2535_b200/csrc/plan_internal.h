@@ -71,6 +71,9 @@ struct moa_fft_plan_s {
     // of n1-point DFTs along the stride-n2 axis, in place on the output
     int64_t n1 = 0, n2 = 0;
     moa_fft_plan_s *rows = nullptr;
+    // low-end breakpoint: the P transforms of length n/p^2 each rank runs on its received
+    // [source][c] blocks (a batched p = 1 plan)
+    moa_fft_plan_s *lowsub = nullptr;
     int t = 0, p = 1, rank = 0, sign = -1, mode = MOA_MODE_LIFTED;
     int d = 0;
     int64_t lift[4] = {0, 0, 0, 0};
@@ -117,6 +120,8 @@ struct moa_fft_plan_s {
     // the last (in, out) pair, captured on a private stream, replayed with one
     // cudaGraphLaunch on the plan stream
     bool graph_ok = false;
+    // low-end breakpoint (options.breakpoint = log2 p + 1): psplit + exchange + local FFT
+    bool lowend = false;
     cudaStream_t graph_stream = nullptr;
     cudaGraphExec_t gexec = nullptr;
     const void *g_in = nullptr;
@@ -144,6 +149,8 @@ namespace moa {
 int default_lifting(int tl, int64_t *lift, int p);
 int choose_T(int logF, int64_t avail);
 int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan> &out);
+// options.breakpoint -> pl->lowend (validation)
+int resolve_breakpoint(moa_fft_plan_s *pl, const moa_fft_options *opt);
 int build_chunked_last(const moa_fft_plan_s *pl, const PassPlan &last, int G, std::vector<PassPlan> &out);
 void free_plan(moa_fft_plan_s *pl);
 int setup_fused(moa_fft_plan_s *pl, int kind);

@@ -327,6 +327,40 @@ def test_emulated_distributed(t, P):
         assert float(np.sqrt(num / den)) <= tol(t), (t, P, sign)
 
 
+@pytest.mark.parametrize("t,P,lift", [(3, 2, None), (5, 2, None), (8, 4, None), (10, 8, None), (14, 4, None),
+                                      (16, 16, None), (20, 2, None), (20, 8, None), (22, 4, [64, 64, 64]),
+                                      (24, 2, None), (24, 8, None)])
+def test_emulated_low_end_breakpoint(t, P, lift):
+    """Fig 5.7 with breakpoint = log2 P + 1 on virtual ranks: psplit (stages
+    1..log2 P + weightcyclic), the exchange, the batched block FFTs and the twiddled
+    P-point combine -- the same X[r + P i] on rank r as the high end, both signs, against
+    the oracle (lift = the block FFTs' lifting, product n/P^2)."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    bp = P.bit_length()
+    for sign in (-1, 1):
+        ref = oracle.fft(x, sign, threads=8)
+        plan = moa.Plan(n, P, sign, mode=moa.MODE_EMULATED, breakpoint=bp, lift=lift)
+        assert plan.info()["breakpoint"] == bp
+        got = _run(plan, xin).reshape(P, n // P)
+        num = den = 0
+        for r in range(P):
+            a, b = oracle.l2_parts(got[r], ref[r::P])
+            num += a
+            den += b
+        assert float(np.sqrt(num / den)) <= tol(t), (t, P, sign)
+
+
+def test_low_end_breakpoint_rejections():
+    with pytest.raises(moa.MoaError, match="NCCL exchange"):
+        moa.Plan(1 << 12, 4, -1, mode=moa.MODE_EMULATED, breakpoint=3, exchange=moa.XCHG_P2P)
+    with pytest.raises(moa.MoaError, match="breakpoint"):
+        moa.Plan(1 << 12, 4, -1, mode=moa.MODE_EMULATED, breakpoint=6)
+    # psize = p: the two ends coincide (log2 p + 1 = log2 psize + 1) -> the high-end path
+    assert moa.Plan(1 << 4, 4, -1, mode=moa.MODE_EMULATED, breakpoint=3).info()["launches"] == 4 * 2
+
+
 @pytest.mark.parametrize("t,P", [(4, 2), (6, 8), (10, 4), (14, 8), (20, 2), (20, 8), (24, 8)])
 def test_emulated_fused_exchange(t, P):
     """MOA_XCHG_P2P on virtual ranks: the last pass stores straight into the destination

@@ -17,14 +17,14 @@ import oracle
 import paper_0811_2535_b200 as moa
 
 
-def replay_local(x_local, n, p, rank, lift=None):
+def replay_local(x_local, n, p, rank, lift=None, breakpoint=0):
     """Run the local passes of one rank from their maps (numpy arithmetic)."""
     m = n // p
     k = 0
     cur = np.asarray(x_local, dtype=np.complex128)
     while True:
         try:
-            F, ii, oi, tw = moa.describe_pass(n, p, rank, k, lift)
+            F, ii, oi, tw = moa.describe_pass(n, p, rank, k, lift, breakpoint)
         except moa.MoaError as e:
             if "outside" in str(e) and k > 0:
                 break
@@ -75,6 +75,48 @@ def test_partitioned_maps_with_exchange(t, p, lift):
         recv = np.concatenate([send[s][d * chunk:(d + 1) * chunk] for s in range(p)])
         out = pcombine(recv, p)
         assert oracle.rel_l2(out, ref[d::p]) <= 1e-13, (d, p)
+
+
+def psplit(x_local, n, p, r):
+    """Low-end phase 1 (test-side numpy): P-point DFTs over x_local[c + chunk*s], times
+    omega_n^((r + p*c)*u), send layout [u][c]."""
+    chunk = x_local.size // p
+    Z = np.fft.fft(np.asarray(x_local).reshape(p, chunk), axis=0)
+    e = ((r + p * np.arange(chunk))[None, :] * np.arange(p)[:, None]) % n
+    return (Z * np.exp(-2j * np.pi * e / n)).reshape(-1)
+
+
+@pytest.mark.parametrize("t,p", [(3, 2), (8, 2), (10, 4), (14, 2), (16, 8), (16, 16), (20, 4)])
+def test_low_end_breakpoint_decomposition(t, p):
+    """The arithmetic the low-end kernels implement (Fig 5.7, breakpoint = log2 p + 1,
+    P:665), in numpy: psplit (P-point DFTs over x_local[c + chunk*s] + the
+    weightcyclic factor omega_n^((r + p*c)*u)), the Fig 5.9 exchange, the p FFTs of
+    length n/p^2 of the received [source][c] blocks, the factor omega_{n/p}^(s*c) and
+    the p-point DFT over s -- X[u + p*v] on rank u, the same as the high end."""
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    ref = oracle.fft(x, -1, threads=8)
+    m = n // p
+    chunk = m // p
+    send = [psplit(x[r::p], n, p, r) for r in range(p)]
+    for u in range(p):
+        recv = np.stack([send[s][u * chunk:(u + 1) * chunk] for s in range(p)])   # [s][c]
+        blocks = np.fft.fft(recv, axis=1)
+        blocks *= np.exp(-2j * np.pi * (np.arange(p)[:, None] * np.arange(chunk)[None, :] % m) / m)
+        got = np.fft.fft(blocks, axis=0).reshape(-1)                               # out[c + chunk*k]
+        assert oracle.rel_l2(got, ref[u::p]) <= 1e-13, (u, p)
+
+
+def test_breakpoint_validation():
+    n = 1 << 12
+    with pytest.raises(moa.MoaError, match="breakpoint"):
+        moa.describe_pass(n, 4, 0, 0, None, 5)        # interior breakpoints are oracle-only
+    with pytest.raises(moa.MoaError, match="breakpoint"):
+        moa.describe_pass(n, 1, 0, 0, None, 1)        # p = 1 has no cyclic phase
+    moa.describe_pass(n, 4, 0, 0, None, 11)           # log2(psize) + 1 = the default
+    with pytest.raises(moa.MoaError, match="batched"):
+        moa.describe_pass(n, 4, 0, 0, None, 3)        # the low end runs a batched p = 1 plan
+    moa.describe_pass(16, 4, 0, 0, None, 3)           # psize = p: both ends are log2 p + 1
 
 
 def test_column_pass_reads_contiguous_runs():

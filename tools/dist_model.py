@@ -22,12 +22,12 @@ import paper_0811_2535_b200 as moa  # noqa: E402
 LINK_GBPS = 770.0
 
 
-def measure(t, P, exchange, reps=10):
+def measure(t, P, exchange, reps=10, breakpoint=0):
     n = 1 << t
     x = torch.empty(n, dtype=torch.complex128, device="cuda")
     moa.gen_uniform(0x08112535 + t, n, x)
     out = torch.empty_like(x)
-    plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=exchange)
+    plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=exchange, breakpoint=breakpoint)
     for _ in range(3):
         plan.execute(x, out)
     torch.cuda.synchronize()
@@ -53,8 +53,9 @@ def main():
     for t in a.t:
         n = 1 << t
         for P in (2, 4, 8):
-            for xname, xchg in (("nccl", moa.XCHG_NCCL), ("p2p", moa.XCHG_P2P)):
-                per_rank, info = measure(t, P, xchg)
+            for xname, xchg, bp in (("nccl", moa.XCHG_NCCL, 0), ("p2p", moa.XCHG_P2P, 0),
+                                    ("nccl, low-end breakpoint", moa.XCHG_NCCL, P.bit_length())):
+                per_rank, info = measure(t, P, xchg, breakpoint=bp)
                 M = n // P
                 a2a_bytes = 16 * M * (P - 1) // P
                 compute = sum(v for k, v in per_rank.items())
@@ -62,12 +63,12 @@ def main():
                 # NCCL: compute, then the exchange, then pcombine (no overlap);
                 # P2P: the exchange is stores of the last pass -> the last pass is bounded
                 # below by its NVLink bytes (overlap inside the kernel)
-                if xname == "nccl":
+                if xname.startswith("nccl"):
                     model = compute + t_a2a
                 else:
                     last = max((v for k, v in per_rank.items() if k.startswith("pass")), default=0.0)
                     model = compute - last + max(last, t_a2a)
-                r = {"t": t, "P": P, "exchange": xname, "lift": info["lift"],
+                r = {"t": t, "P": P, "exchange": xname, "lift": info["lift"], "breakpoint": info["breakpoint"],
                      "per_rank_kernels_us": {k: round(v, 1) for k, v in per_rank.items()},
                      "per_rank_compute_us": round(compute, 1), "a2a_bytes_per_rank": a2a_bytes,
                      "a2a_us_model_at_770GBps": round(t_a2a, 1), "per_gpu_us_model": round(model, 1),
@@ -82,7 +83,9 @@ def main():
                     "emulated launches); the all-to-all is MODELLED as bytes / 770 GB/s (measured NVLink "
                     "peer copy, B200_PROFILING.md). NCCL: compute + exchange, no overlap. P2P: the last "
                     "pass stores into the peers, so it is bounded below by its NVLink bytes. These are "
-                    "projections, not multi-GPU measurements.\n\n")
+                    "projections, not multi-GPU measurements. The low-end breakpoint (SURVEY N4, P:694) "
+                    "runs psplit (the first log2 p stages + weightcyclic) before the exchange and the "
+                    "whole local FFT after it.\n\n")
             f.write("| n | p | exchange | lifting (n/p) | per-rank kernels (µs) | exchange B/rank | "
                     "exchange µs (model) | per-GPU µs (model) | GFLOP/s (model) |\n"
                     "|---|---|---|---|---|---|---|---|---|\n")
