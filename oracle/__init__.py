@@ -13,6 +13,8 @@ paper figure it follows (P:<line> of PAPER.md, arXiv 0811.2535):
 * ``fft_temp``  -- Fig 3.8, temporary ``xx``
 * ``dft``       -- the plain definition X_k = sum_j x_j w^{jk}, O(n^2), long double
 * ``dft_bins``  -- the same definition at selected bins (sampled parity at large n)
+* ``dft_bins_range`` -- its sum over one window x[j0 : j0+len] (windows of a partition add
+                   up to ``dft_bins``; streams inputs larger than host memory)
 * ``bitrev``    -- P_n, Fig 2.1 line 1
 * ``weights``   -- weight(row) = EXP(sign 2 pi i row / L) (Fig 3.8)
 * ``dist_sim``  -- Fig 5.7 + Fig 5.9 with m virtual processors
@@ -63,6 +65,7 @@ def _load():
             lib.oracle_fft_temp.argtypes = [i64, ctypes.c_int, dp, dp]
             lib.oracle_dft.argtypes = [i64, ctypes.c_int, dp, dp]
             lib.oracle_dft_bins.argtypes = [i64, ctypes.c_int, dp, i64, ctypes.POINTER(i64), dp]
+            lib.oracle_dft_bins_range.argtypes = [i64, ctypes.c_int, dp, i64, i64, i64, ctypes.POINTER(i64), dp]
             lib.oracle_bitrev.argtypes = [i64, dp, dp]
             lib.oracle_weights.argtypes = [i64, ctypes.c_int, dp]
             lib.oracle_omega.argtypes = [i64, i64, ctypes.c_int, dp]
@@ -121,6 +124,18 @@ def dft_bins(x, ks, sign: int = -1) -> np.ndarray:
     rc = lib.oracle_dft_bins(x.size, sign, _dp(x), ks.size,
                              ks.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(out))
     _check(rc, "dft_bins")
+    return out
+
+
+def dft_bins_range(x_window, n: int, j0: int, ks, sign: int = -1) -> np.ndarray:
+    """The plain definition restricted to x[j0 : j0 + len(x_window)]: summing the
+    windows of a partition of [0, n) gives dft_bins (inputs too large for host memory)."""
+    x = _c128(x_window)
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int64))
+    out = np.empty(ks.size, dtype=np.complex128)
+    rc = _load().oracle_dft_bins_range(int(n), sign, _dp(x), int(j0), x.size, ks.size,
+                                       ks.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(out))
+    _check(rc, "dft_bins_range")
     return out
 
 

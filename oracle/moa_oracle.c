@@ -311,6 +311,58 @@ int oracle_dft_bins(int64_t n, int sign, const double *in, int64_t nk, const int
 }
 
 /*
+ * The plain definition restricted to a window of the input:
+ *   out_b = sum_{j=0}^{len-1} x[j0 + j] * omega_n^(sign * k_b * (j0 + j)),
+ * with in = x + j0 (len elements).  Summing the windows of a partition of [0, n)
+ * gives dft_bins; it lets a test stream an input too large for host memory.
+ */
+int oracle_dft_bins_range(int64_t n, int sign, const double *in, int64_t j0, int64_t len, int64_t nk,
+                          const int64_t *ks, double *out) {
+    int t = log2_exact(n);
+    if (t < 0 || (sign != 1 && sign != -1) || j0 < 0 || len < 0 || j0 + len > n) return ORACLE_EINVAL;
+    int h = (t + 1) / 2;
+    int64_t nlo = (int64_t)1 << h, nhi = n >> h;
+    long double *Wlo = (long double *)malloc(sizeof(long double) * 2 * (size_t)nlo);
+    long double *Whi = (long double *)malloc(sizeof(long double) * 2 * (size_t)nhi);
+    if (!Wlo || !Whi) {
+        free(Wlo); free(Whi);
+        return ORACLE_ENOMEM;
+    }
+    const long double two_pi = 6.2831853071795864769252867665590058L;
+    const long double sg = sign < 0 ? -1.0L : 1.0L;
+    for (int64_t e = 0; e < nlo; ++e) {
+        long double a = two_pi * (long double)e / (long double)n;
+        Wlo[2 * e] = cosl(a);
+        Wlo[2 * e + 1] = sg * sinl(a);
+    }
+    for (int64_t e = 0; e < nhi; ++e) {
+        long double a = two_pi * (long double)(e << h) / (long double)n;
+        Whi[2 * e] = cosl(a);
+        Whi[2 * e + 1] = sg * sinl(a);
+    }
+    for (int64_t b = 0; b < nk; ++b) {
+        int64_t k = ks[b] & (n - 1);
+        long double sr = 0.0L, si = 0.0L;
+        /* (j0 + j)*k mod n, updated incrementally (128-bit start: j0*k can exceed 2^63) */
+        uint64_t e = (uint64_t)(((unsigned __int128)(uint64_t)j0 * (uint64_t)k) & (unsigned __int128)(n - 1));
+        for (int64_t j = 0; j < len; ++j) {
+            const long double *wl = &Wlo[2 * (e & (uint64_t)(nlo - 1))];
+            const long double *wh = &Whi[2 * (e >> h)];
+            long double wr = wh[0] * wl[0] - wh[1] * wl[1];
+            long double wi = wh[0] * wl[1] + wh[1] * wl[0];
+            long double xr = in[2 * j], xi = in[2 * j + 1];
+            sr += xr * wr - xi * wi;
+            si += xr * wi + xi * wr;
+            e = (e + (uint64_t)k) & (uint64_t)(n - 1);
+        }
+        out[2 * b] = (double)sr;
+        out[2 * b + 1] = (double)si;
+    }
+    free(Wlo); free(Whi);
+    return ORACLE_OK;
+}
+
+/*
  * Fig 5.7 per-processor template with partitioned data, with the
  * direct block-partitioned -> cyclic-partitioned redistribution of Fig 5.9
  * (P:1047-1062), simulated for m virtual processors run one after another.

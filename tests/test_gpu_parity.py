@@ -470,3 +470,41 @@ def test_config_2_30_sampled_bins():
     lhs = torch.sum(out.abs() ** 2).item()
     rhs = n * torch.sum(x.abs() ** 2).item()
     assert abs(lhs - rhs) / rhs <= 1e-12
+
+
+@pytest.mark.slow
+def test_max_size_2_31():
+    """The largest transform one B200 holds with its own scratch: n = 2^31 (in + out +
+    scratch = 96 GiB), where element offsets inside a pass reach 2^31 and byte offsets
+    2^35.  Sampled bins against the plain definition streamed through the host in 1 GiB
+    windows (oracle.dft_bins_range), Parseval on the whole output, and the in-place
+    device round trip FFT_+1(FFT_-1 x)/n = x."""
+    t = 31
+    n = 1 << t
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(moa_inputs.seed_for(t), n, x)
+    plan = moa.Plan(n)
+    assert plan.info()["passes"] == 4
+    out = plan.execute(x)
+    torch.cuda.synchronize()
+    plan.destroy()
+    ks = np.array([0, 1, 3, (1 << 30) + 7, 123456789, n - 1])
+    got = out[torch.from_numpy(ks).cuda()].cpu().numpy()
+    win = 1 << 26
+    ref = np.zeros(ks.size, dtype=np.complex128)
+    for j0 in range(0, n, win):
+        ref += oracle.dft_bins_range(x[j0:j0 + win].cpu().numpy(), n, j0, ks)
+    assert oracle.rel_l2(got, ref) <= tol(t)
+    lhs = sum(torch.sum(out[j0:j0 + win].abs() ** 2).item() for j0 in range(0, n, win))
+    rhs = n * sum(torch.sum(x[j0:j0 + win].abs() ** 2).item() for j0 in range(0, n, win))
+    assert abs(lhs - rhs) / rhs <= 1e-12
+    inv = moa.Plan(n, 1, +1)
+    inv.execute(out, out)
+    torch.cuda.synchronize()
+    inv.destroy()
+    num = den = 0.0
+    for j0 in range(0, n, win):
+        num += torch.sum((out[j0:j0 + win] / n - x[j0:j0 + win]).abs() ** 2).item()
+        den += torch.sum(x[j0:j0 + win].abs() ** 2).item()
+    assert (num / den) ** 0.5 <= 2 * tol(t)
+

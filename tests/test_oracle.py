@@ -138,6 +138,27 @@ def test_dft_bins_equals_definition():
     assert oracle.rel_l2(oracle.dft_bins(x, ks), np.fft.fft(x)[ks]) <= 1e-14
 
 
+def test_dft_bins_range_windows_sum_to_the_definition():
+    """Windows of a partition of [0, n) sum to the plain definition (numpy's FFT as the
+    independent check), including a window start whose j0*k exceeds 2^63 (the 128-bit
+    start exponent); a lone impulse at j0 gives omega_n^(k*j0) exactly."""
+    t = 14
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    ks = [0, 1, 5, 4097, n // 2, n - 1]
+    for sign in SIGNS:
+        acc = sum(oracle.dft_bins_range(x[j0:j0 + 1024], n, j0, ks, sign) for j0 in range(0, n, 1024))
+        ref = np.fft.fft(x)[ks] if sign < 0 else np.fft.ifft(x)[ks] * n
+        assert oracle.rel_l2(acc, ref) <= 1e-14
+    # impulse at j0 of a 2^40-point signal, bins near 2^40: (j0 * k) >> 63 != 0
+    n = 1 << 40
+    j0 = (1 << 40) - 3
+    ks = np.array([(1 << 40) - 1, (1 << 39) + 12345, 3])
+    got = oracle.dft_bins_range(np.array([1.0 + 0j]), n, j0, ks)
+    want = np.exp(-2j * np.pi * ((j0 * ks) % n) / n)
+    assert np.max(np.abs(got - want)) <= 1e-15
+
+
 def test_dft_non_power_of_two_against_numpy():
     # the definition itself, for lengths the FFT cannot take
     for n in (1, 3, 5, 6, 7, 12, 31):
