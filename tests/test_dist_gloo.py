@@ -132,3 +132,64 @@ def test_centralized_cyclic_layouts_over_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res[r] is True for r in range(world)), res
+
+
+def _block_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import moa_inputs
+        import oracle
+        import paper_0811_2535_b200 as moa
+        from test_plan_maps import pcombine, replay_local
+        t = 12
+        n = 1 << t
+        p = world
+        m = n // p
+        chunk = m // p
+        x = moa_inputs.signal_for(t)
+        xb = torch.from_numpy(x[rank * m:(rank + 1) * m].copy())
+        xc = moa.block_to_cyclic(xb)                                     # Fig 5.3 / 5.9 direct
+        ok_direct = np.array_equal(xc.numpy(), x[rank::p])
+        xv = moa.block_to_cyclic_via_central(xb)                         # Fig 5.4 via processor 0
+        ok_central = np.array_equal(xv.numpy(), x[rank::p])
+        # the partitioned transform on the cyclic slice (product maps + a real exchange),
+        # then the output back to natural blocks: X[r*psize : (r+1)*psize]
+        send = replay_local(xc.numpy(), n, p, rank)
+        recv = torch.empty(2 * m, dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(send.view(np.float64).copy()),
+                               [2 * chunk] * p, [2 * chunk] * p)
+        Xc = torch.from_numpy(pcombine(recv.numpy().view(np.complex128), p).copy())
+        Xb = moa.cyclic_to_block(Xc)
+        ref = oracle.fft(x, -1)
+        err = oracle.rel_l2(Xb.numpy(), ref[rank * m:(rank + 1) * m])
+        q.put((rank, (ok_direct, ok_central, err)))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_block_natural_layouts_over_gloo(world):
+    """block-natural input and output around the cyclic transform
+    (block_to_cyclic, cyclic_to_block: one all-to-all each) and Fig 5.4's via-central
+    redistribution (gather to processor 0, scatter back: 2(m-1) messages) -- both give
+    rank r exactly x[r::p]; the natural blocks of the result equal the oracle's X."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        ok_direct, ok_central, err = res[r]
+        assert ok_direct and ok_central, (r, res[r])
+        assert err <= 1e-13, (r, err)
+
