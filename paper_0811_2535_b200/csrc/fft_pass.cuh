@@ -207,6 +207,25 @@ __host__ __device__ constexpr int lrs(int F) {
     return F / ns;
 }
 
+// NS of the stage that wrote the exchange read by the stage starting at NS (0: none)
+__host__ __device__ constexpr int writer_ns(int F, int NS) {
+    int ns = 1;
+    if (NS <= 1) return 0;
+    while (ns * stage_radix(F, ns) < NS) ns *= stage_radix(F, ns);
+    return ns;
+}
+// Extra bank-group XOR for an exchange written by a radix-16 stage with NS = 2 or 4 (the
+// stage after a radix-2/4 remainder stage, F = 512, 1024, 8192): its quarter-warp lanes
+// differ in point bits {0, 5, 6} (NS = 2) or {0, 1, 6} (NS = 4), which swz() maps onto 4
+// bank groups; bit 6 goes to the bank bit swz leaves constant (tools/bank_sim.py:
+// F = 1024 stores 2.0 -> 1.0 wavefronts per ideal in that stage, no other pattern changes).
+template <int NSW>
+__device__ __forceinline__ int xmask(int f) {
+    if constexpr (NSW == 4) return ((f >> 6) & 1) << 2;
+    if constexpr (NSW == 2) return ((f >> 6) & 1) << 1;
+    return 0;
+}
+
 template <int F, int T>
 struct PassShape {
     static constexpr int R = F >= MOA_RMAX ? MOA_RMAX : F;   // points per thread
@@ -457,9 +476,11 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         for (int i = 0; i < M; ++i) {
             const int j = jj[i];
             if constexpr (NB >= 8) {
+                constexpr int NSW = writer_ns(F, NS);
                 const int rowoff = tt[i] * ROW, pj = j ^ swz(j);
 #pragma unroll
-                for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[rowoff + ((pj ^ swz(r * NB)) + r * NB)];
+                for (int r = 0; r < RS; ++r)
+                    x[i * RS + r] = sm[rowoff + ((pj ^ swz(r * NB) ^ xmask<NSW>(j + r * NB)) + r * NB)];
             } else {
 #pragma unroll
                 for (int r = 0; r < RS; ++r) x[i * RS + r] = sm[smem_idx<F, T>(tt[i], j + r * NB)];
@@ -496,6 +517,13 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
                 const int sb = swz(base);
 #pragma unroll
                 for (int r = 0; r < RS; ++r) sm[pb + (r ^ sb ^ swz(r))] = x[i * RS + r];
+            } else if constexpr (NS == 2 || NS == 4) {
+                const int rowoff = tt[i] * ROW;
+#pragma unroll
+                for (int r = 0; r < RS; ++r) {
+                    const int f = base + r * NS;
+                    sm[rowoff + (f ^ swz(f) ^ xmask<NS>(f))] = x[i * RS + r];
+                }
             } else {
 #pragma unroll
                 for (int r = 0; r < RS; ++r) sm[smem_idx<F, T>(tt[i], base + r * NS)] = x[i * RS + r];
