@@ -1,8 +1,8 @@
 """C5 size sweep: forward complex128 FFT for n = 2^t, t = 4..30 on one GPU.
 
-For every t: plan (default lifting), 3 warm-up executes, then REPS executes timed one by
-one with CUDA events on the plan stream, with a 1 GiB L2 flush before each (so
-L2-resident sizes are reported L2-cold; the L2-hot median is reported beside it).
+For every t: plan (default lifting), 3 warm-up executes, then back-to-back batches timed
+with one CUDA event pair each (see run()): L2-hot, and L2-cold (1 GiB flush before every
+execute, the flush-only batch subtracted).
 Prints one JSON line per size and, with --md PATH, writes the markdown table.
 
     python tools/sweep.py --tmin 4 --tmax 30 --md profiles/r01_sweep.md
@@ -28,7 +28,24 @@ def peaks():
         return 6650.0
 
 
+def _span(s, fn, reps):
+    """seconds between two events around `reps` calls of fn on stream s."""
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        fn()
+    b.record(s)
+    b.synchronize()
+    return a.elapsed_time(b) * 1e-3
+
+
 def run(t, reps):
+    """This box's CUDA event clock ticks in 2.048 us steps, so a transform of t <= 20 is
+    not timed alone: 'hot' = one event pair around `reps` back-to-back executes, 'cold' =
+    (reps x [1 GiB L2 flush + execute]) - (reps x flush), both / reps, median of 5.  From
+    2^21 on: the median of `reps` executes each between its own event pair (after a flush
+    for 'cold')."""
     n = 1 << t
     x = torch.empty(n, dtype=torch.complex128, device="cuda")
     moa.gen_uniform(moa_inputs.seed_for(t), n, x)
@@ -39,18 +56,28 @@ def run(t, reps):
     with torch.cuda.stream(s):
         for _ in range(3):
             plan.execute(x, out)
-        cold, hot = [], []
-        for flush, acc in ((True, cold), (False, hot)):
+
+        def fft():
+            plan.execute(x, out)
+
+        def flush():
+            fl.fill_(1.0)
+
+        def both():
+            fl.fill_(1.0)
+            plan.execute(x, out)
+
+        hot, cold = [], []
+        if t <= 20:   # shorter than ~10 event ticks: batches
+            for _ in range(5):
+                hot.append(_span(s, fft, reps) / reps)
+                cold.append((_span(s, both, reps) - _span(s, flush, reps)) / reps)
+        else:         # one event pair per execute (tick <= 5 % of the transform)
             for _ in range(reps):
-                if flush:
-                    fl.fill_(1.0)
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(s)
-                plan.execute(x, out)
-                b.record(s)
-                b.synchronize()
-                acc.append(a.elapsed_time(b) * 1e-3)
+                flush()
+                cold.append(_span(s, fft, 1))
+            for _ in range(reps):
+                hot.append(_span(s, fft, 1))
     info = plan.info()
     plan.destroy()
     cold.sort()
@@ -72,7 +99,7 @@ def main():
     pk = peaks()
     rows = []
     for t in range(a.tmin, a.tmax + 1):
-        reps = 20 if t <= 26 else 5
+        reps = 20 if t <= 26 else 3
         r = run(t, reps)
         r["frac_of_measured_hbm"] = round(r["alg_GBps_cold"] / pk, 3)
         rows.append(r)
@@ -81,13 +108,13 @@ def main():
     if a.md:
         with open(a.md, "w") as f:
             f.write("# C5 size sweep, 1 B200, forward complex128 (default liftings)\n\n")
-            f.write(f"Median of 20 (t <= 26) or 5 executes; L2 flushed (1 GiB write) before each 'cold' "
-                    f"execute, none before 'hot'. GFLOP/s = 5 n log2 n / t. alg GB/s = 32 n x HBM passes / t; "
-                    f"fraction of the measured {pk} GB/s copy peak (MEASURED_PEAKS.json). Sizes <= 2^13 run "
-                    f"in one CTA (latency-bound); up to ~2^22 the data is L2-resident between passes. "
-                    f"For launch-bound sizes the 'hot' column includes the CPU submission latency (the GPU "
-                    f"is idle when the transform is launched), while in the 'cold' column the preceding flush "
-                    f"kernel hides it.\n\n")
+            f.write(f"This box's CUDA event clock ticks in 2.048 us steps. t <= 20: 'hot' = one event pair "
+                    f"around 20 back-to-back executes / 20; 'cold' = (20 x [1 GiB L2 flush + execute] minus "
+                    f"20 x flush) / 20; median of 5 (for t <= ~15 'hot' is the CPU submission rate of "
+                    f"back-to-back calls, 'cold' the GPU time). t >= 21: median of 20 (t <= 26) or 3 "
+                    f"executes, each between its own event pair, after a flush for 'cold'. GFLOP/s = 5 n log2 n / t. alg GB/s = 32 n x HBM passes / t; fraction of "
+                    f"the measured {pk} GB/s copy peak (MEASURED_PEAKS.json). Sizes <= 2^12 run in one CTA "
+                    f"(latency-bound); up to ~2^22 the data is L2-resident between passes.\n\n")
             f.write("| t | lifting | launches | us (cold) | us (hot) | GFLOP/s (cold) | GFLOP/s (hot) | alg GB/s | "
                     "frac HBM |\n|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
