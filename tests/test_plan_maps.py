@@ -158,7 +158,9 @@ def test_default_lifting_table_every_t_and_p():
             if p > 1 and len(lift) > 1:
                 assert lift[0] >= p, (t, p, lift)
     assert moa.default_lifting(1 << 24) == [256, 256, 256]
-    assert moa.default_lifting(1 << 20) == [1024, 1024]
+    assert moa.default_lifting(1 << 20) == [256, 4096]
+    assert moa.default_lifting(1 << 15) == [256, 128]
+    assert moa.default_lifting(1 << 21, 2) == [1024, 1024]   # p > 1 keeps <2^(tl/2), 2^(tl/2)>
     assert moa.default_lifting(1 << 21) == [128, 256, 64]
     assert moa.default_lifting(1 << 22) == [128, 256, 128]
     assert moa.default_lifting(1 << 23) == [128, 256, 256]

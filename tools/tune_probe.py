@@ -16,6 +16,43 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import perf_probe  # noqa: E402
 
 
+def time_batched(t, lift, reps=20):
+    """L2-cold time of one execute below the 2.048 us event tick: (reps x [1 GiB flush +
+    execute] - reps x flush) / reps, median of 3 (tools/sweep.py's method)."""
+    import torch
+    import paper_0811_2535_b200 as moa
+    n = 1 << t
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(0x08112535 + t, n, x)
+    out = torch.empty_like(x)
+    plan = moa.Plan(n, lift=lift)
+    fl = torch.empty(1 << 28, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+
+    def span(fn):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            fn()
+        b.record(s)
+        b.synchronize()
+        return a.elapsed_time(b) * 1e-3
+
+    for _ in range(3):
+        plan.execute(x, out)
+    ts = []
+    for _ in range(3):
+        both = span(lambda: (fl.fill_(1.0), plan.execute(x, out)))
+        only = span(lambda: fl.fill_(1.0))
+        ts.append((both - only) / reps)
+    ts.sort()
+    info = plan.info()
+    plan.destroy()
+    return {"t": t, "lift": info["lift"], "us": round(ts[1] * 1e6, 2), "us_min": round(ts[0] * 1e6, 2),
+            "tf": os.environ.get("MOA_FFT_TF", "default"), "kernels": []}
+
+
 def liftings(t):
     out = []
     for a in range(max(1, t - 13), min(13, t - 1) + 1):
@@ -56,7 +93,7 @@ def main():
                     os.environ["MOA_FFT_MINTILES"] = str(mt)
                     os.environ["MOA_FFT_TF"] = str(tf)
                 try:
-                    r = perf_probe.time_plan(t, lift, reps=3 if big else 10)
+                    r = (perf_probe.time_plan(t, lift, reps=3) if big else time_batched(t, lift))
                 except Exception as e:   # unsupported (F, T) combination
                     print(json.dumps({"t": t, "lift": lift, "mintiles": mt, "tf": tf, "error": str(e)[:80]}))
                     continue
@@ -66,7 +103,7 @@ def main():
                     best = r
         os.environ.pop("MOA_FFT_MINTILES", None)
         os.environ.pop("MOA_FFT_TF", None)
-        d = perf_probe.time_plan(t, None, reps=10)
+        d = perf_probe.time_plan(t, None, reps=3) if big else time_batched(t, None)
         print(json.dumps({"t": t, "default": d["lift"], "default_us": d["us"], "best": best["lift"],
                           "best_us": best["us"], "best_mintiles": best["mintiles"], "best_tf": best["tf"]}),
               flush=True)
