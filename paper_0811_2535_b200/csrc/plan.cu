@@ -898,7 +898,10 @@ int make_plan_nd(int rank, const int64_t *shape, int sign, moa_fft_plan_s **res)
         for (int l = 0; l < a; ++l) A *= shape[l];
         for (int l = a + 1; l < rank; ++l) B *= shape[l];
         const int64_t N = shape[a];
-        if (N <= FMAX) {   // one pass, in place: view [A][N][B]
+        // one in-place pass while its column tiles keep >= 64-byte runs (T >= 4); longer
+        // axes as two lifted passes (2-D 4096 x 4096: columns 205 -> 2 x ~87 us; 8192 x 8192:
+        // one T = 1 pass of 16-byte runs took 1216 us, tools/nd_probe.py)
+        if (N <= 1024) {   // one pass, in place: view [A][N][B]
             PassPlan pp = axis_pass(ilog2(N), B);
             PassDesc &D = pp.d;
             D.nmask = (uint64_t)N - 1;
