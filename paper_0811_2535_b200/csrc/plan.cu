@@ -340,6 +340,15 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
                 pp.tiles = D.U * D.V * (d >= 3 ? Fv[1] : 1);
             } else {
                 int T = fill_T(choose_T(pp.logF, Fv[0]), pl->M / F, pl->batch);
+                // 256-byte output runs (T = 16, 2 tiles per SM) when the transposed store's
+                // rows are >= 1 MiB apart (MOA_FFT_WIDE_LAST, bytes; 0 = off): 2^24 pass 2
+                // 91.4 -> 90.4 us, step 258.6 -> 256.8 us (bench, 3 alternating runs)
+                {
+                    const int wl = env_int("MOA_FFT_WIDE_LAST", 1 << 20);
+                    if (wl > 0 && P == 1 && pp.logF == 8 && (int64_t)16 * Kk >= wl && T == (2048 >> pp.logF) &&
+                        2 * T <= Fv[0] && pass_supported(pp.logF, 2 * T) && pl->batch == 1)
+                        T *= 2;
+                }
                 pp.T = T;
                 D.U = Fv[0] / T;
                 D.V = d >= 3 ? Fv[1] : 1;
