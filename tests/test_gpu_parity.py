@@ -352,6 +352,19 @@ def test_emulated_low_end_breakpoint(t, P, lift):
         assert float(np.sqrt(num / den)) <= tol(t), (t, P, sign)
 
 
+def test_low_end_breakpoint_in_place_and_repeated():
+    """The low end in place (out = in) over three executes of one plan, equal to the
+    out-of-place result bit for bit (psplit consumes the input before anything is written)."""
+    t, P = 16, 4
+    n = 1 << t
+    x = moa_inputs.signal_for(t)
+    xin = np.concatenate([x[r::P] for r in range(P)])
+    plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, breakpoint=3)
+    ref = _run(plan, xin)
+    for _ in range(3):
+        assert np.array_equal(_run(plan, xin, inplace=True), ref)
+
+
 def test_low_end_breakpoint_rejections():
     with pytest.raises(moa.MoaError, match="NCCL exchange"):
         moa.Plan(1 << 12, 4, -1, mode=moa.MODE_EMULATED, breakpoint=3, exchange=moa.XCHG_P2P)
