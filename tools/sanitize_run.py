@@ -40,6 +40,16 @@ def main():
         got = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=xchg).execute(xin).view(P, -1)
         for r in range(P):
             check(got[r], ref[r::P], ("emulated", xchg, r))
+    got = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, breakpoint=3).execute(xin).view(P, -1)   # low end
+    for r in range(P):
+        check(got[r], ref[r::P], ("emulated low-end", r))
+    for t in (9, 10):   # radix-2/4 remainder stages (xmask exchanges), row and column tiles
+        m = 1 << t
+        y = torch.randn(4 * m * m, dtype=torch.complex128, device="cuda")
+        check(moa.Plan(m * m, lift=[m, m]).execute(y[:m * m]), torch.fft.fft(y[:m * m]), ("remainder", t))
+        check(moa.Plan(m, batch=4 * m).execute(y), torch.fft.fft(y.view(4 * m, m)).reshape(-1), ("rem-batch", t))
+    y = torch.randn(4096, 64, dtype=torch.complex128, device="cuda")
+    check(moa.Plan2D(4096, 64).execute(y).view(4096, 64), torch.fft.fft2(y), "2d long column axis")
     got = moa.Plan(1 << 10, mode=moa.MODE_LITERAL).execute(x[:1024])
     check(got, torch.fft.fft(x[:1024]), "literal")
     print("sanitize_run ok")
