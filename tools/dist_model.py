@@ -94,6 +94,20 @@ def main():
                 f.write(f"| 2^{r['t']} | {r['P']} | {r['exchange']} | {'x'.join(map(str, r['lift']))} | {ks} | "
                         f"{r['a2a_bytes_per_rank']} | {r['a2a_us_model_at_770GBps']} | {r['per_gpu_us_model']} | "
                         f"{r['GFLOPs_model']} |\n")
+            f.write("\n## N2: Fig 5.9 direct vs Fig 5.4 via-central redistribution (MODEL)\n\n"
+                    "Bytes / 770 GB/s per link direction. Direct (Fig 5.9, P:1043): every rank sends "
+                    "(m-1)/m of its psize elements to the others at once. Via central (Fig 5.4, P:844): "
+                    "processor 0 receives (m-1) blocks of psize and sends (m-1) cyclic slices of psize "
+                    "through its own link: 2(m-1) messages, every element moved twice, rank 0's link "
+                    "the bottleneck (its two directions overlap: max of in and out).\n\n"
+                    "| n | p | direct µs | via central µs | ratio |\n|---|---|---|---|---|\n")
+            for t in a.t:
+                n = 1 << t
+                for P in (2, 4, 8):
+                    M = n // P
+                    direct = 16 * M * (P - 1) / P / (LINK_GBPS * 1e9) * 1e6
+                    central = 16 * M * (P - 1) / (LINK_GBPS * 1e9) * 1e6   # rank 0: (m-1) psize each way
+                    f.write(f"| 2^{t} | {P} | {direct:.1f} | {central:.1f} | {central / direct:.1f}x |\n")
 
 
 if __name__ == "__main__":
