@@ -117,3 +117,28 @@ def test_nd_plan_validation_errors(shape, needle):
     with pytest.raises(moa.MoaError) as e:
         moa.PlanND(shape)
     assert needle in str(e.value), str(e.value)
+
+
+def test_binding_structs_match_the_header_layout(tmp_path):
+    """The ctypes mirrors of moa_fft_options / moa_fft_info / moa_fft_kernel_stat have the
+    size and field offsets the C compiler gives the header's structs (an ABI drift check:
+    a field added on one side only would shift every later field)."""
+    fields = {"moa_fft_options": moa._Options, "moa_fft_info": moa._Info, "moa_fft_kernel_stat": moa._KernelStat}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "moa_fft.h"', "int main(void) {"]
+    for cname, py in fields.items():
+        lines.append(f'    printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'    printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["    return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"),
+                           "-I", "/usr/local/cuda/include", str(src), "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in fields.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
