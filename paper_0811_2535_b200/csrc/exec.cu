@@ -59,7 +59,8 @@ int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, dou
         D.peer_off = peer_off;
     }
     char name[64];
-    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx, pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : ""),
+    snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx,
+             pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : (pp.tmast && !peers ? "_tmast" : "")),
              1 << pp.logF, pp.T,
              peers ? "+push" : "");
     ProfScope ps_(pl, name, 32 * pl->M * pl->batch);
@@ -70,6 +71,12 @@ int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, dou
             if (rc) return rc;
         }
         e = launch_pass_tma(pp.logF, pp.T, pp.tma, D, pp.map, pp.tiles, pp.tma_grid, pl->stream);
+    } else if (pp.tmast && !peers) {
+        if (pp.omap_base != (const void *)dst) {
+            int rc = encode_out_map(pp, dst);
+            if (rc) return rc;
+        }
+        e = launch_pass_tmast(pp.logF, pp.T, D, pp.omap, pp.tiles, pl->stream);
     } else if (pp.pf_grid > 0) {
         e = launch_pass_pf(pp.logF, pp.T, D, pp.tiles, pp.pf_grid, pl->stream);
     } else {

@@ -38,6 +38,23 @@ cudaError_t MOA_CAT(launch_pass_f, MOA_INST_LOGF)(int T, const PassDesc &d, int6
     }
 }
 
+// row pass with bulk-tensor stores (ST = 4): F >= 256, 2T doubles per box row
+cudaError_t MOA_CAT(launch_pass_tmast_f, MOA_INST_LOGF)(int T, const PassDesc &d, const CUtensorMap &omap,
+                                                       int64_t tiles, cudaStream_t s) {
+#define MOA_TMAST_CASE(TT)                                                                       \
+    if (T == TT) {                                                                               \
+        if constexpr (kF >= 256 && TT * kF <= TF_MAX) return launch_tmast<kF, TT>(d, omap, tiles, s); \
+        return cudaErrorInvalidValue;                                                            \
+    }
+    MOA_TMAST_CASE(1)
+    MOA_TMAST_CASE(2)
+    MOA_TMAST_CASE(4)
+    MOA_TMAST_CASE(8)
+    MOA_TMAST_CASE(16)
+#undef MOA_TMAST_CASE
+    return cudaErrorInvalidValue;
+}
+
 // TMA-staged persistent variants: F >= 32, T*F <= 4096 (staging + exchange buffers fit)
 template <int T, int SRC>
 static constexpr bool tma_ok() {

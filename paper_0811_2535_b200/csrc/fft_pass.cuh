@@ -300,6 +300,12 @@ __device__ __forceinline__ int stage_idx(int t, int f) {
     }
 }
 
+// ST = 4: the last stage's output tensor map (a no-op hook otherwise)
+struct OMapHook {
+    const CUtensorMap *m;
+    __device__ __forceinline__ void operator()() const {}
+};
+
 struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
@@ -532,6 +538,7 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
         __syncthreads();
     } else {
         const uint32_t so = (uint32_t)NB * (uint32_t)d.out_k;
+        if constexpr (ST == 4) __syncthreads();   // every lane has read the exchange buffer
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const int t = tt[i], j = jj[i];
@@ -549,6 +556,11 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
 #pragma unroll
                 for (int r = 0; r < RS; ++r) v[r].y = -v[r].y;
             }
+            if constexpr (ST == 4) {   // stage [k][t] for the bulk-tensor store
+#pragma unroll
+                for (int r = 0; r < RS; ++r) sm[(j + r * NB) * T + t] = v[r];
+                continue;
+            }
             if (d.pack_lp >= 0) {   // general pack (single-level local transform, p > 1)
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
@@ -562,6 +574,19 @@ __device__ __forceinline__ void fft_stage(double2 *x, double2 *sm, const PassDes
                 double2 *po = elem_off(c.out, (uint32_t)t * (uint32_t)d.out_t + (uint32_t)j * (uint32_t)d.out_k);
 #pragma unroll
                 for (int r = 0; r < RS; ++r) st_io<ST>(elem_off_c(po, r, so), v[r], pol);
+            }
+        }
+        if constexpr (ST == 4) {
+            // boxes of KB k-rows x T points: output inner index c.k_base + t (runs of T),
+            // outer index k (stride K_k); one thread hands them to the TMA engine
+            constexpr int KB = F < 256 ? F : 256;
+            fence_proxy_async();
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll 1
+                for (int kb = 0; kb < F / KB; ++kb)
+                    tma_store_2d(hook.m, sm + kb * KB * T, 2 * (int)c.k_base, kb * KB);
+                tma_store_drain();
             }
         }
     }
@@ -617,6 +642,44 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
     tile_fft<F, T, 0, NoHook, 0, 0, TW>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH), d, io,
                    blockIdx.x);
+}
+
+// Row pass whose transposed store goes through shared memory and the TMA engine
+// (cp.async.bulk.tensor stores of KB k-rows x T points) instead of per-lane st.global.
+template <int F, int T, int TW>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_tmast_kernel(const PassDesc d, const __grid_constant__ CUtensorMap omap) {
+    extern __shared__ double2 sm[];
+    if (d.pdl) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    tile_fft<F, T, 0, OMapHook, 0, 4, TW>(sm, reinterpret_cast<double2 *>(reinterpret_cast<char *>(sm) + PassShape<F, T>::XCH),
+                                          d, io, blockIdx.x, nullptr, OMapHook{&omap});
+}
+
+template <int F, int T>
+cudaError_t launch_tmast(const PassDesc &d, const CUtensorMap &omap, int64_t tiles, cudaStream_t s) {
+    using SH = PassShape<F, T>;
+    auto kernel = d.twiddle ? fft_pass_tmast_kernel<F, T, 1> : fft_pass_tmast_kernel<F, T, 0>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tiles);
+    cfg.blockDim = dim3(SH::NT);
+    cfg.dynamicSmemBytes = SH::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = d.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, d, omap);
 }
 
 // ---------------------------------------------------------------------------

@@ -48,6 +48,20 @@ cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaS
     }
 }
 
+cudaError_t launch_pass_tmast(int logF, int T, const PassDesc &d, const CUtensorMap &omap, int64_t tiles,
+                              cudaStream_t s) {
+    if (tiles <= 0 || tiles > 0x7fffffffll) return cudaErrorInvalidValue;
+    switch (logF) {
+    case 8: return launch_pass_tmast_f8(T, d, omap, tiles, s);
+    case 9: return launch_pass_tmast_f9(T, d, omap, tiles, s);
+    case 10: return launch_pass_tmast_f10(T, d, omap, tiles, s);
+    case 11: return launch_pass_tmast_f11(T, d, omap, tiles, s);
+    case 12: return launch_pass_tmast_f12(T, d, omap, tiles, s);
+    case 13: return launch_pass_tmast_f13(T, d, omap, tiles, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 int pass_tma_grid(int logF, int T, int src) {
     switch (logF) {
     case 5: return grid_pass_tma_f5(T, src);

@@ -93,6 +93,9 @@ int pass_supported(int logF, int T);
 size_t pass_smem_bytes(int logF, int T);
 int pass_threads(int logF, int T);
 cudaError_t launch_pass(int logF, int T, const PassDesc &d, int64_t tiles, cudaStream_t s);
+// the row pass with its transposed store issued as bulk-tensor stores from shared memory
+cudaError_t launch_pass_tmast(int logF, int T, const PassDesc &d, const CUtensorMap &omap, int64_t tiles,
+                              cudaStream_t s);
 cudaError_t prepare_pass_kernels();    // raise the dynamic smem limits once
 // TMA-staged persistent pass (src 1: column tile, 2: row tile); grid 0 = unsupported
 int pass_tma_grid(int logF, int T, int src);
@@ -141,6 +144,8 @@ cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int
     int grid_pass_tma_f##f(int T, int src);                                                 \
     cudaError_t launch_pass_pf_f##f(int T, const PassDesc &d, int64_t tiles, int grid, cudaStream_t s); \
     int grid_pass_pf_f##f(int T);                                                           \
+    cudaError_t launch_pass_tmast_f##f(int T, const PassDesc &d, const CUtensorMap &omap, int64_t tiles, \
+                                       cudaStream_t s);                                     \
     }
 MOA_DECLARE_INST(1)
 MOA_DECLARE_INST(2)

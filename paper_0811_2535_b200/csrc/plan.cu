@@ -126,6 +126,22 @@ int encode_pass_map(PassPlan &pp, const void *base) {
     return MOA_OK;
 }
 
+// output map of a bulk-tensor-store last pass: dims {2*K_k doubles (inner index), F (k)}
+int encode_out_map(PassPlan &pp, const void *base) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const PassDesc &D = pp.d;
+    const uint64_t F = 1ull << pp.logF, T = pp.T, Kk = (uint64_t)D.K_k;
+    cuuint64_t dims[2] = {2 * Kk, F}, strides[1] = {16 * Kk};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * T), (cuuint32_t)(F < 256 ? F : 256)}, estr[2] = {1, 1};
+    CUresult r = enc(&pp.omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for the output map", (int)r);
+    pp.omap_base = base;
+    return MOA_OK;
+}
+
 // choose the TMA-staged variant when it exists for this (F, T, layout), else the
 // prefetching persistent kernel when selected
 void choose_tma(PassPlan &pp) {
@@ -783,6 +799,19 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         }
         if (batch == 1)
             for (auto &pp : pl->passes) choose_tma(pp);
+        // bulk-tensor stores for the row pass from F = 1024 on (MOA_FFT_TMAST = minimum log2 F,
+        // 0 = off): the per-lane transposed stores of T <= 4 rows throttle the LSU; measured
+        // 2^26 F = 1024 403 -> 384 us, 2^27 F = 2048 964 -> 841 us, 2^28 F = 4096 2345 -> 2323 us;
+        // slower at F = 256 (90.5 -> 102) and 512 (190 -> 194), whose T >= 8 runs do not
+        const int tmast_min = env_int("MOA_FFT_TMAST", 10);
+        if (p == 1 && batch == 1 && tmast_min > 0 && !pl->passes.empty()) {
+            PassPlan &lp = pl->passes.back();
+            const PassDesc &D = lp.d;
+            if (D.last && lp.logF >= tmast_min && lp.logF >= 8 && !lp.tma && !lp.pf_grid && D.pack_lp < 0 &&
+                D.K_t == 1 && D.out_t == 1 && D.out_k == D.K_k && D.out_u == D.K_u && D.out_v == D.K_v &&
+                D.out_w == D.K_w && 2 * lp.T <= 256)
+                lp.tmast = 1;
+        }
         const int fuse = batch == 1 ? env_int("MOA_FFT_FUSE", 0) : 0;
         if (p == 1 && pl->d == 3 && fuse && (rc = setup_fused(pl, fuse)) != MOA_OK) {
             free_plan(pl);

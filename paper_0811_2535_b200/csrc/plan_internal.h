@@ -53,6 +53,9 @@ struct PassPlan {
     int tma = 0;
     int tma_grid = 0;
     int pf_grid = 0;   // > 0: prefetching persistent kernel (fft_pass_pf_kernel)
+    int tmast = 0;     // last pass stores through the TMA engine (launch_pass_tmast)
+    CUtensorMap omap;  // its output map (encoded for omap_base)
+    const void *omap_base = nullptr;
     int io = 0;        // r-D axis passes: 0 = out -> out (in place), 1 = out -> work, 2 = work -> out
     CUtensorMap map;
     const void *map_base = nullptr;
@@ -155,6 +158,7 @@ int build_chunked_last(const moa_fft_plan_s *pl, const PassPlan &last, int G, st
 void free_plan(moa_fft_plan_s *pl);
 int setup_fused(moa_fft_plan_s *pl, int kind);
 int resolve_lifting(moa_fft_plan_s *pl, const moa_fft_options *opt);
+int encode_out_map(PassPlan &pp, const void *base);
 int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_plan_s **res);
 int make_plan_nd(int rank, const int64_t *shape, int sign, moa_fft_plan_s **res);
 

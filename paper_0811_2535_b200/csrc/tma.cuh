@@ -61,4 +61,20 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// shared -> global bulk-tensor store (bulk-group completion): the TMA engine scatters
+// the box's rows, not the LSU
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+
+// commit the issued bulk stores and wait until they have completed (the dependent pass
+// or the caller reads them right after the grid)
+__device__ __forceinline__ void tma_store_drain() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // (.read: -1 % at 2^26 only)
+}
+
 }  // namespace moa
