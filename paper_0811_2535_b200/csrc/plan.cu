@@ -804,7 +804,8 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         // 2^26 F = 1024 403 -> 384 us, 2^27 F = 2048 964 -> 841 us, 2^28 F = 4096 2345 -> 2323 us;
         // slower at F = 256 (90.5 -> 102) and 512 (190 -> 194), whose T >= 8 runs do not
         const int tmast_min = env_int("MOA_FFT_TMAST", 10);
-        if (p == 1 && batch == 1 && tmast_min > 0 && !pl->passes.empty()) {
+        if (p == 1 && batch == 1 && tmast_min > 0 && pl->M >= ((int64_t)1 << 22) && !pl->passes.empty()) {
+            // (HBM-sized transforms only: at 2^19 / 2^20 it measured equal or slower)
             PassPlan &lp = pl->passes.back();
             const PassDesc &D = lp.d;
             if (D.last && lp.logF >= tmast_min && lp.logF >= 8 && !lp.tma && !lp.pf_grid && D.pack_lp < 0 &&
