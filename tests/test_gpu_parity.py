@@ -521,3 +521,32 @@ def test_max_size_2_31():
         den += torch.sum(x[j0:j0 + win].abs() ** 2).item()
     assert (num / den) ** 0.5 <= 2 * tol(t)
 
+
+def test_tma_store_row_pass_bitwise_and_offsets(monkeypatch):
+    """The bulk-tensor-store row pass (F >= 1024, HBM-sized transforms) writes exactly what
+    the per-lane stores write: bitwise equal for an output 16 bytes past an allocation
+    boundary (TMA needs only 16-byte alignment), in place, and against the oracle."""
+    t = 25
+    n = 1 << t
+    lift = [128, 256, 1024]
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(moa_inputs.seed_for(t), n, x)
+    monkeypatch.setenv("MOA_FFT_TMAST", "0")
+    ref = moa.Plan(n, lift=lift).execute(x)
+    monkeypatch.setenv("MOA_FFT_TMAST", "10")
+    plan = moa.Plan(n, lift=lift)
+    buf = torch.empty(n + 1, dtype=torch.complex128, device="cuda")
+    plan.set_profiling(True)
+    got = plan.execute(x, buf[1:])
+    torch.cuda.synchronize()
+    assert any("fft_pass_tmast" in k["name"] for k in plan.get_profile())   # the TMA-store kernel ran
+    plan.set_profiling(False)
+    assert torch.equal(got, ref)
+    y = x.clone()
+    plan.execute(y, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    ks = np.array([0, 1, 12345, n // 2 + 3, n - 1])
+    assert oracle.rel_l2(ref[torch.from_numpy(ks).cuda()].cpu().numpy(),
+                         oracle.dft_bins(x.cpu().numpy(), ks)) <= tol(t)
+
