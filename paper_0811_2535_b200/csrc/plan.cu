@@ -356,6 +356,13 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
                 pp.tiles = D.U * D.V * (d >= 3 ? Fv[1] : 1);
             } else {
                 int T = fill_T(choose_T(pp.logF, Fv[0]), pl->M / F, pl->batch);
+                // with bulk-tensor stores (make_plan: MOA_FFT_TMAST) the 512- and 1024-point row
+                // passes take 2048-element tiles (4 CTAs/SM): the TMA engine scatters their
+                // 64- / 32-byte runs (2^25 F = 512 190 -> 175 us, 2^26 F = 1024 384 -> 355 us)
+                if (P == 1 && pl->batch == 1 && pl->M >= ((int64_t)1 << 22) && (pp.logF == 9 || pp.logF == 10) &&
+                    env_int("MOA_FFT_TMAST", 9) > 0 && env_int("MOA_FFT_TMAST", 9) <= pp.logF &&
+                    (T << pp.logF) > 2048 && pass_supported(pp.logF, 2048 >> pp.logF))
+                    T = 2048 >> pp.logF;
                 // 256-byte output runs (T = 16, 2 tiles per SM) when the transposed store's
                 // rows are >= 1 MiB apart (MOA_FFT_WIDE_LAST, bytes; 0 = off): 2^24 pass 2
                 // 91.4 -> 90.4 us, step 258.6 -> 256.8 us (bench, 3 alternating runs)
@@ -799,11 +806,12 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         }
         if (batch == 1)
             for (auto &pp : pl->passes) choose_tma(pp);
-        // bulk-tensor stores for the row pass from F = 1024 on (MOA_FFT_TMAST = minimum log2 F,
+        // bulk-tensor stores for the row pass from F = 512 on (MOA_FFT_TMAST = minimum log2 F,
         // 0 = off): the per-lane transposed stores of T <= 4 rows throttle the LSU; measured
-        // 2^26 F = 1024 403 -> 384 us, 2^27 F = 2048 964 -> 841 us, 2^28 F = 4096 2345 -> 2323 us;
-        // slower at F = 256 (90.5 -> 102) and 512 (190 -> 194), whose T >= 8 runs do not
-        const int tmast_min = env_int("MOA_FFT_TMAST", 10);
+        // 2^26 F = 1024 403 -> 384 us (T = 4; 355 us at T = 2), 2^27 F = 2048 964 -> 841 us,
+        // 2^28 F = 4096 2345 -> 2323 us; slower at F = 256 (90.5 -> 102, T = 16) and at
+        // F = 512 with T = 8 (190 -> 194; T = 4 gives 175)
+        const int tmast_min = env_int("MOA_FFT_TMAST", 9);
         if (p == 1 && batch == 1 && tmast_min > 0 && pl->M >= ((int64_t)1 << 22) && !pl->passes.empty()) {
             // (HBM-sized transforms only: at 2^19 / 2^20 it measured equal or slower)
             PassPlan &lp = pl->passes.back();
