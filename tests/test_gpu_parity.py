@@ -205,7 +205,7 @@ def test_plan_info():
     info = moa.Plan(1 << 28).info()
     assert info["passes"] == 3 and info["lift"] == [256, 256, 4096]
     info = moa.Plan(1 << 29).info()   # four levels from 2^29 (DESIGN.md §4 lifting table)
-    assert info["passes"] == 4 and info["lift"] == [64, 128, 256, 256]
+    assert info["passes"] == 4 and info["lift"] == [128, 128, 128, 256]
 
 
 @pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"}, {"MOA_FFT_PF": "1"}, {"MOA_FFT_PF": "3"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "2"}, {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])

@@ -166,4 +166,5 @@ def test_default_lifting_table_every_t_and_p():
     assert moa.default_lifting(1 << 23) == [128, 256, 256]
     assert moa.default_lifting(1 << 26) == [256, 256, 1024]
     assert moa.default_lifting(1 << 30) == [128, 128, 256, 256]
+    assert moa.default_lifting(1 << 29) == [128, 128, 128, 256]
     assert moa.default_lifting(1 << 10) == [1024]
