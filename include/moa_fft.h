@@ -138,7 +138,7 @@ moa_fft_plan_t moa_fft_plan(int64_t n, int p, int sign);
  * operation to every sub-array along an axis (B.1-B.6), so the 2-D DFT
  *   X[k1][k2] = sum_{j1,j2} x[j1][j2] exp(sign*2*pi*i*(j1*k1/n1 + j2*k2/n2))
  * is the lifted 1-D FFT over the rows followed by the same over the columns.
- *   n1 = 2^t1, 1 <= t1 <= 26 (the column transforms: one pass up to 2^13, else two
+ *   n1 = 2^t1, 1 <= t1 <= 26 (the column transforms: one pass up to 2^10, else two
  *   lifted passes), n2 = 2^t2 with t2 >= 1 (the rows: a batched lifted 1-D plan),
  *   n1 * n2 <= 2^32.
  * x, X: n1 x n2 complex128, row-major (element (j1, j2) at j1*n2 + j2).  Execute
@@ -151,7 +151,7 @@ moa_fft_plan_t moa_fft_plan_2d(int64_t n1, int64_t n2, int sign);
  * complex128 array: X[k] = sum_j x[j] exp(sign*2*pi*i * sum_a j_a*k_a/shape[a]).
  * The last axis is any power of two (a batched lifted 1-D plan); every other axis is
  * 2^t with 1 <= t <= 26: one pass of DFTs along that strided axis, in place, for
- * t <= 13, else two lifted passes through a plan-owned work buffer (twiddle
+ * t <= 10, else two lifted passes through a plan-owned work buffer (twiddle
  * omega_N^(j2*k1) between them, transposed store); last-but-one axis first.  The
  * product of the extents is <= 2^32.  Execute
  * with moa_fft_execute; in == out allowed.  NULL on error.  (moa_fft_plan_2d is the
@@ -174,7 +174,8 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
  * Single-GPU multi-pass plans replay their kernel launches as one CUDA graph per
  * (in, out) pair: the first execute with a new pair captures it (on a private
  * stream) and launches it; the graph only remembers the pointer values, so the
- * caller may free or reuse the buffers afterwards ($MOA_FFT_GRAPH=0 disables it).
+ * caller may free or reuse the buffers afterwards.  (Tuning knobs: every MOA_FFT_*
+ * environment variable -- e.g. MOA_FFT_GRAPH=0 -- is ignored unless MOA_FFT_ABLATION=1.)
  * Returns MOA_OK or MOA_ERR_ALIGN / MOA_ERR_CUDA / MOA_ERR_NCCL.
  */
 int moa_fft_execute(moa_fft_plan_t plan, const void *in, void *out);
@@ -286,8 +287,15 @@ int moa_fft_execute_phase(moa_fft_plan_t plan, const void *in, void *out, int ph
  */
 int moa_fft_default_lifting(int64_t n, int p, int64_t *lift_out, int *d_out);
 
-/* Thread-local description of the last error ("" if none). */
+/* Thread-local description of the last error ("" if none), naming the violated bound
+ * for argument errors. */
 const char *moa_fft_last_error(void);
+
+/* Thread-local MOA_ERR_* code of the last error (MOA_OK if none): the code that
+ * accompanies moa_fft_last_error()'s message, also for calls that return a plan
+ * (NULL) rather than a code.  E.g. moa_fft_plan(6, 1, -1) -> NULL and
+ * moa_fft_last_error_code() == MOA_ERR_INVALID_N. */
+int moa_fft_last_error_code(void);
 
 /*
  * Distributed setup: one library-owned NCCL communicator per process, created

@@ -57,7 +57,7 @@ EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execut
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
            "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase",
-           "moa_fft_plan_2d", "moa_fft_plan_nd", "moa_fft_default_lifting"]
+           "moa_fft_plan_2d", "moa_fft_plan_nd", "moa_fft_default_lifting", "moa_fft_last_error_code"]
 
 _lib = None
 
@@ -67,11 +67,12 @@ def lib_path() -> str:
 
 
 def load(build_if_needed: bool = True):
-    """Load libmoa_fft.so (building it with nvcc first only if it is missing)."""
+    """Load libmoa_fft.so, (re)building it with nvcc first when it is missing or older
+    than any of its sources (build.needs_build), so a stale library is never loaded."""
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_needed and not os.path.exists(_build.LIB):
+    if build_if_needed and _build.needs_build():
         _build.build()
     if not os.path.exists(_build.LIB):
         raise ImportError(f"{_build.LIB} is missing; run paper_0811_2535_b200/build.py (no CPU fallback)")
@@ -98,6 +99,7 @@ def load(build_if_needed: bool = True):
     lib.moa_fft_set_stream.argtypes = [vp, vp]
     lib.moa_fft_plan_info.argtypes = [vp, ctypes.POINTER(_Info)]
     lib.moa_fft_last_error.restype = ctypes.c_char_p
+    lib.moa_fft_last_error_code.restype = ctypes.c_int
     lib.moa_dist_unique_id.argtypes = [vp]
     lib.moa_dist_init.argtypes = [ci, ci, vp]
     lib.moa_gen_uniform.argtypes = [ctypes.c_uint64, i64, i64, i64, vp, vp]
@@ -114,8 +116,23 @@ def _err(code: int):
     raise MoaError(code, _lib.moa_fft_last_error().decode())
 
 
+def _plan_err(lib):
+    """A plan constructor returned NULL: raise with the library's own MOA_ERR_* code."""
+    code = int(lib.moa_fft_last_error_code()) or -9
+    raise MoaError(code, lib.moa_fft_last_error().decode())
+
+
 def _ptr(x) -> int:
     return x if isinstance(x, int) else int(x.data_ptr())
+
+
+def _cur_device():
+    """The CUDA device plans bind to (torch's current device), None without CUDA."""
+    try:
+        import torch
+        return int(torch.cuda.current_device()) if torch.cuda.is_available() else None
+    except Exception:  # pragma: no cover
+        return None
 
 
 def _cur_stream() -> int:
@@ -150,10 +167,11 @@ class Plan:
                 opt.lift[i] = int(f)
         h = lib.moa_fft_plan_ex(int(n), int(p), int(sign), ctypes.byref(opt))
         if not h:
-            raise MoaError(-9, lib.moa_fft_last_error().decode())
+            _plan_err(lib)
         self._h = h
+        self.device = _cur_device()
         self.n, self.p, self.sign, self.mode = int(n), int(p), int(sign), mode
-        self.exchange, self.rank, self.batch = int(exchange), int(rank), int(batch)
+        self.exchange, self.rank, self.batch = int(exchange), int(rank), max(1, int(batch))
         self._stream = None
         self.set_stream(stream)
 
@@ -183,11 +201,39 @@ class Plan:
         d["lift"] = [int(v) for v in inf.lift[: inf.passes]] if self.mode != MODE_LITERAL else []
         return d
 
+    def expected_elems(self) -> int:
+        """Elements one execute reads and writes: batch*n (p = 1), n/p per rank, or all p
+        ranks' slices back to back (EMULATED)."""
+        if self.p == 1:
+            return self.n * self.batch
+        return self.n if self.mode == MODE_EMULATED else self.n // self.p
+
+    def _check(self, x, what: str):
+        """A tensor argument must be a contiguous complex128 CUDA tensor on the plan's
+        device holding exactly expected_elems() elements (raw pointers are passed as is)."""
+        if isinstance(x, int):
+            return
+        import torch
+        if not isinstance(x, torch.Tensor):
+            raise TypeError(f"{what} must be a torch tensor or a raw device pointer (int)")
+        if x.dtype != torch.complex128:
+            raise ValueError(f"{what} has dtype {x.dtype}; the transform is complex128")
+        if not x.is_cuda or (self.device is not None and x.device.index != self.device):
+            raise ValueError(f"{what} must live on cuda:{self.device} (got {x.device})")
+        if not x.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if x.numel() != self.expected_elems():
+            raise ValueError(f"{what} holds {x.numel()} elements; this plan transforms {self.expected_elems()}")
+
     def execute(self, x, out=None):
         """Transform device data x (torch complex128 tensor or raw pointer) into out."""
         if out is None:
             import torch
+            if isinstance(x, int):
+                raise ValueError("out is required when x is a raw pointer")
             out = torch.empty_like(x)
+        self._check(x, "x")
+        self._check(out, "out")
         rc = _lib.moa_fft_execute(self._h, _ptr(x), _ptr(out))
         if rc:
             _err(rc)
@@ -286,8 +332,9 @@ class Plan2D(Plan):
         lib = load()
         h = lib.moa_fft_plan_2d(int(n1), int(n2), int(sign))
         if not h:
-            raise MoaError(-9, lib.moa_fft_last_error().decode())
+            _plan_err(lib)
         self._h = h
+        self.device = _cur_device()
         self.n1, self.n2 = int(n1), int(n2)
         self.n, self.p, self.sign, self.mode = self.n1 * self.n2, 1, int(sign), MODE_LIFTED
         self.exchange, self.rank, self.batch = XCHG_NCCL, 0, 1
@@ -304,8 +351,9 @@ class PlanND(Plan):
         shp = (ctypes.c_int64 * len(shape))(*[int(v) for v in shape])
         h = lib.moa_fft_plan_nd(len(shape), shp, int(sign))
         if not h:
-            raise MoaError(-9, lib.moa_fft_last_error().decode())
+            _plan_err(lib)
         self._h = h
+        self.device = _cur_device()
         self.shape = tuple(int(v) for v in shape)
         n = 1
         for v in self.shape:

@@ -14,8 +14,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build" + os.environ.get("MOA_BUILD_TAG", ""))
-LIB = os.environ.get("MOA_FFT_LIB") or os.path.join(HERE, "libmoa_fft.so")
+# MOA_BUILD_VARIANTS=1: the ablation library libmoa_fft_variants.so, which also holds the
+# pass variants measured slower and kept out of the product (persistent / TMA-staged /
+# prefetching passes, the L2-fused pass pair), selected only through the
+# MOA_FFT_* knobs under MOA_FFT_ABLATION=1.  The default build is the product library.
+VARIANTS = os.environ.get("MOA_BUILD_VARIANTS", "0") not in ("", "0")
+BUILD = os.path.join(HERE, "_build" + ("_variants" if VARIANTS else "") + os.environ.get("MOA_BUILD_TAG", ""))
+LIB = os.environ.get("MOA_FFT_LIB") or os.path.join(HERE, "libmoa_fft_variants.so" if VARIANTS else "libmoa_fft.so")
+VARIANTS_LIB = os.path.join(HERE, "libmoa_fft_variants.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -23,7 +29,9 @@ FLAGS = [*os.environ.get("MOA_NVCC_EXTRA", "").split(),
          "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"]
 
-SOURCES = ["kernels.cu", "plan.cu", "exec.cu", "abi.cu", "dist.cu", "fused.cu"]
+SOURCES = ["kernels.cu", "plan.cu", "exec.cu", "abi.cu", "dist.cu"] + (["fused.cu"] if VARIANTS else [])
+if VARIANTS:
+    FLAGS.append("-DMOA_VARIANTS=1")
 INST_LOGF = list(range(1, 14))
 
 
@@ -70,6 +78,17 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     if verbose:
         print(f"built {LIB}", file=sys.stderr)
     return LIB
+
+
+def build_variants(force: bool = False) -> str:
+    """Build libmoa_fft_variants.so (the ablation library) in a child process."""
+    env = dict(os.environ, MOA_BUILD_VARIANTS="1")
+    env.pop("MOA_FFT_LIB", None)
+    cmd = [sys.executable, os.path.abspath(__file__)] + (["--force"] if force else [])
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"variants build failed:\n{r.stdout}\n{r.stderr}")
+    return VARIANTS_LIB
 
 
 if __name__ == "__main__":

@@ -48,9 +48,22 @@ int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
     return rc;
 }
 
+// switch to the plan's device for the lifetime of a call, restoring the caller's
+struct DeviceGuard {
+    int cur = 0, dev = 0;
+    explicit DeviceGuard(int d) : dev(d) {
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (cur != dev) cudaSetDevice(cur);
+    }
+};
+
 int moa_fft_execute_host(moa_fft_plan_t pl, const void *host_in, void *host_out) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
     if (!host_in || !host_out) return fail(MOA_ERR_ALIGN, "NULL host buffer");
+    DeviceGuard guard_(pl->device);   // staging buffers and copies on the plan's device
     int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M * pl->batch;
     size_t bytes = (size_t)elems * sizeof(double2);
     if (!pl->stage_in) {
@@ -76,15 +89,7 @@ int moa_fft_execute_host_batch(moa_fft_plan_t pl, int count, const void *const *
     for (int i = 0; i < count; ++i)
         if (!host_in[i] || !host_out[i]) return fail(MOA_ERR_ALIGN, "NULL host buffer at batch index %d", i);
     if (count == 0) return MOA_OK;
-    int cur = 0;
-    cudaGetDevice(&cur);
-    if (cur != pl->device) cudaSetDevice(pl->device);
-    struct Restore {
-        int cur, dev;
-        ~Restore() {
-            if (cur != dev) cudaSetDevice(cur);
-        }
-    } restore_{cur, pl->device};
+    DeviceGuard guard_(pl->device);
     int64_t elems = (pl->mode == MOA_MODE_EMULATED) ? pl->n : pl->M * pl->batch;
     size_t bytes = (size_t)elems * sizeof(double2);
     if (!pl->stage_in) {
@@ -284,6 +289,8 @@ int moa_fft_plan_info(moa_fft_plan_t pl, moa_fft_info *o) {
 }
 
 const char *moa_fft_last_error(void) { return last_error(); }
+
+int moa_fft_last_error_code(void) { return last_error_code(); }
 
 int moa_fft_describe_pass(int64_t n, int p, int rank, const moa_fft_options *opts, int pass, int64_t *in_idx,
                           int64_t *out_idx, int64_t *tw_exp, int64_t *F_out) {

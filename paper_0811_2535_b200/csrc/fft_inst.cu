@@ -55,6 +55,7 @@ cudaError_t MOA_CAT(launch_pass_tmast_f, MOA_INST_LOGF)(int T, const PassDesc &d
     return cudaErrorInvalidValue;
 }
 
+#ifdef MOA_VARIANTS
 // TMA-staged persistent variants: F >= 32, T*F <= 4096 (staging + exchange buffers fit)
 template <int T, int SRC>
 static constexpr bool tma_ok() {
@@ -141,6 +142,8 @@ int MOA_CAT(grid_pass_pf_f, MOA_INST_LOGF)(int T) {
 #undef MOA_PF_GRID
     return 0;
 }
+
+#endif  // MOA_VARIANTS
 
 cudaError_t MOA_CAT(prepare_pass_f, MOA_INST_LOGF)() {
     cudaError_t e;

@@ -663,12 +663,7 @@ template <int F, int T>
 cudaError_t launch_tmast(const PassDesc &d, const CUtensorMap &omap, int64_t tiles, cudaStream_t s) {
     using SH = PassShape<F, T>;
     auto kernel = d.twiddle ? fft_pass_tmast_kernel<F, T, 1> : fft_pass_tmast_kernel<F, T, 0>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        attr = true;
-    }
+    // (the shared-memory limit is raised per device by prepare_one, plan.cu)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tiles);
     cfg.blockDim = dim3(SH::NT);
@@ -682,6 +677,7 @@ cudaError_t launch_tmast(const PassDesc &d, const CUtensorMap &omap, int64_t til
     return cudaLaunchKernelEx(&cfg, kernel, d, omap);
 }
 
+#ifdef MOA_VARIANTS
 // ---------------------------------------------------------------------------
 // Persistent pass with the next tile prefetched into the exchange buffer.
 // The exchange buffer is idle from the moment the last stage has read it until
@@ -858,6 +854,8 @@ int grid_one_pf() {
     return per_sm * sms;
 }
 
+#endif  // MOA_VARIANTS
+
 template <int F, int T>
 cudaError_t launch_one(const PassDesc &d, int64_t tiles, cudaStream_t s) {
     using SH = PassShape<F, T>;
@@ -886,14 +884,22 @@ cudaError_t prepare_one() {
         cudaError_t e = cudaFuncSetAttribute(fft_pass_kernel<F, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)SH::SMEM);
         if (e != cudaSuccess) return e;
-        return cudaFuncSetAttribute(fft_pass_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)SH::SMEM);
+        e = cudaFuncSetAttribute(fft_pass_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        if (e != cudaSuccess) return e;
+        if constexpr (F >= 256 && T <= 16) {   // the bulk-tensor-store row pass (launch_tmast)
+            e = cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SH::SMEM);
+            if (e != cudaSuccess) return e;
+            return cudaFuncSetAttribute(fft_pass_tmast_kernel<F, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)SH::SMEM);
+        }
     }
     return cudaSuccess;
 }
 
 }  // namespace moa
 
+#ifdef MOA_VARIANTS
 namespace moa {
 
 // ---------------------------------------------------------------------------
@@ -1080,3 +1086,4 @@ int grid_one_tma() {
 }
 
 }  // namespace moa
+#endif  // MOA_VARIANTS

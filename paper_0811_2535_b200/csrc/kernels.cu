@@ -6,7 +6,26 @@
 //   gen_uniform        the SplitMix64 input recipe (test/bench helper, no FFT arithmetic)
 #include "fft_pass.cuh"
 
+#include <atomic>
+
 namespace moa {
+
+// SM count of the current device (queried once per device, then cached)
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev].load() <= 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 1;
+        }
+        cache[dev].store(v);
+    }
+    return cache[dev].load();
+}
 
 // ------------------------------------------------------------------ dispatcher
 int pass_supported(int logF, int T) {
@@ -62,6 +81,7 @@ cudaError_t launch_pass_tmast(int logF, int T, const PassDesc &d, const CUtensor
     }
 }
 
+#ifdef MOA_VARIANTS
 int pass_tma_grid(int logF, int T, int src) {
     switch (logF) {
     case 5: return grid_pass_tma_f5(T, src);
@@ -120,6 +140,24 @@ cudaError_t launch_pass_pf(int logF, int T, const PassDesc &d, int64_t tiles, in
     default: return cudaErrorInvalidValue;
     }
 }
+
+#else
+// product build: the persistent / TMA-staged / prefetching pass variants and the
+// L2-fused pass pair were measured slower and are compiled only into
+// libmoa_fft_variants.so (MOA_BUILD_VARIANTS=1); the plan never selects them here
+int pass_tma_grid(int, int, int) { return 0; }
+cudaError_t launch_pass_tma(int, int, int, const PassDesc &, const CUtensorMap &, int64_t, int, cudaStream_t) {
+    return cudaErrorInvalidValue;
+}
+int pass_pf_grid(int, int) { return 0; }
+cudaError_t launch_pass_pf(int, int, const PassDesc &, int64_t, int, cudaStream_t) { return cudaErrorInvalidValue; }
+int fused_supported(int, int, int, int) { return 0; }
+cudaError_t launch_fused(int, int, int, int, const FusedDesc &, const CUtensorMap &, const CUtensorMap &, int,
+                         cudaStream_t) {
+    return cudaErrorInvalidValue;
+}
+int fused_grid(int, int, int, int) { return 0; }
+#endif
 
 cudaError_t prepare_pass_kernels() {
     cudaError_t (*fns[])() = {prepare_pass_f1, prepare_pass_f2, prepare_pass_f3, prepare_pass_f4,
@@ -211,7 +249,7 @@ cudaError_t launch_radix2_stage(const double2 *in, double2 *out, int t, int q, c
                                 const double2 *tw_lo, int hbits, int conj_out, cudaStream_t s) {
     uint64_t half = 1ull << (t - 1);
     uint64_t blocks = (half + 255) / 256;
-    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    if (blocks > (uint64_t)sm_count() * 64) blocks = (uint64_t)sm_count() * 64;
     radix2_stage_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, out, t, q, tw_hi, tw_lo, hbits, conj_out);
     return cudaGetLastError();
 }
@@ -256,9 +294,7 @@ __global__ void __launch_bounds__(256) pcombine_kernel(const double2 *__restrict
 cudaError_t launch_pcombine(const double2 *recv, double2 *out, int64_t chunk, int P, int conj_out,
                             cudaStream_t s) {
     // one wave of 8 CTAs of 256 threads per SM, each thread U columns per sweep
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     int64_t blocks = (chunk + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     switch (P) {
@@ -304,9 +340,7 @@ __global__ void __launch_bounds__(256) psplit_kernel(const double2 *__restrict__
 
 cudaError_t launch_psplit(const double2 *in, double2 *send, int64_t chunk, int P, int64_t r, int64_t n,
                           const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_in, cudaStream_t s) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     int64_t blocks = (chunk + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     const uint64_t nm = (uint64_t)n - 1;
@@ -353,9 +387,7 @@ __global__ void __launch_bounds__(256) pcombine_tw_kernel(const double2 *__restr
 
 cudaError_t launch_pcombine_tw(const double2 *recv, double2 *out, int64_t chunk, int P, int64_t n,
                                const double2 *tw_hi, const double2 *tw_lo, int hbits, int conj_out, cudaStream_t s) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     int64_t blocks = (chunk + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     const uint64_t nm = (uint64_t)n - 1;
@@ -400,7 +432,7 @@ cudaError_t launch_pcombine_chunk(const double2 *recv, double2 *out, int64_t cou
     while (((int64_t)1 << li) < inner_len) ++li;
     while (((int64_t)1 << lwg) < wg) ++lwg;
     int64_t blocks = (count + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
     switch (P) {
     case 2: pcombine_chunk_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
     case 4: pcombine_chunk_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(recv, out, count, li, lwg, f1, goff, out_stride, conj_out); break;
@@ -433,7 +465,7 @@ cudaError_t launch_gen_uniform(uint64_t seed, int64_t first, int64_t stride, int
                                cudaStream_t s) {
     if (count <= 0) return cudaSuccess;
     int64_t blocks = (count + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > (int64_t)sm_count() * 32) blocks = (int64_t)sm_count() * 32;
     gen_uniform_kernel<<<(unsigned)blocks, 256, 0, s>>>(seed, first, stride, count, out);
     return cudaGetLastError();
 }

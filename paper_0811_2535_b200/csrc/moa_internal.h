@@ -89,6 +89,7 @@ struct FusedDesc {
 };
 
 // host-side launchers (kernels.cu / fft_inst.cu)
+int sm_count();   // SM count of the current device (cached per device)
 int pass_supported(int logF, int T);
 size_t pass_smem_bytes(int logF, int T);
 int pass_threads(int logF, int T);

@@ -15,15 +15,22 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "plan_internal.h"
 
 namespace moa {
 
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_err;
+static thread_local int g_code = MOA_OK;
 
-void clear_error() { g_err.clear(); }
+void clear_error() {
+    g_err.clear();
+    g_code = MOA_OK;
+}
 const char *last_error() { return g_err.c_str(); }
+int last_error_code() { return g_code; }
 
 int fail(int code, const char *fmt, ...) {
     char buf[512];
@@ -32,6 +39,7 @@ int fail(int code, const char *fmt, ...) {
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
     g_err = buf;
+    g_code = code;
     return code;
 }
 
@@ -147,14 +155,17 @@ int encode_out_map(PassPlan &pp, const void *base) {
 void choose_tma(PassPlan &pp) {
     pp.tma = 0;
     pp.pf_grid = 0;
-    const char *pf_env = getenv("MOA_FFT_PF");
-    if (pf_env && atoi(pf_env) && pp.logF >= 5) {
+#ifndef MOA_VARIANTS
+    (void)pp;
+    return;   // the persistent / TMA-staged variants live in libmoa_fft_variants.so only
+#else
+    const int pf_env = env_int("MOA_FFT_PF", 0);
+    if (pf_env && pp.logF >= 5) {
         int g = pass_pf_grid(pp.logF, pp.T);
         if (g > 0) pp.pf_grid = (int)(g < pp.tiles ? g : pp.tiles);
     }
-    const char *tma_env = getenv("MOA_FFT_TMA");   // 1: double-buffered TMA, 2: single buffer + prefetch
-    if (!tma_env || atoi(tma_env) == 0) return;
-    const int tma_kind = atoi(tma_env);
+    const int tma_kind = env_int("MOA_FFT_TMA", 0);   // 1: double-buffered TMA, 2: single buffer + prefetch
+    if (tma_kind == 0) return;
     const PassDesc &D = pp.d;
     int src = 0;
     if (!D.last && D.in_t == 1 && pp.T >= 2) src = 1;
@@ -165,6 +176,7 @@ void choose_tma(PassPlan &pp) {
     if (g <= 0) return;
     pp.tma = code;
     pp.tma_grid = g;
+#endif
 }
 
 // default lifting <F1..Fd> of a local length 2^tl, from the B200 lifting sweeps
@@ -725,6 +737,10 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
             so.nlift = opt->nlift;
             for (int i = 0; i < opt->nlift && i < 4; ++i) so.lift[i] = opt->lift[i];
         }
+        if (exchange != MOA_XCHG_NCCL) {   // (checked before the sub-plan owns device memory)
+            delete pl;
+            return fail(MOA_ERR_INVALID_ARG, "the low-end breakpoint runs with the NCCL exchange (or EMULATED ranks)");
+        }
         if ((rc0 = make_plan(pl->M / p, 1, -1, &so, &pl->lowsub)) != MOA_OK) {
             delete pl;
             return rc0;
@@ -734,10 +750,6 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
     } else if ((rc0 = resolve_lifting(pl, opt)) != MOA_OK) {
         delete pl;
         return rc0;
-    }
-    if (pl->lowend && exchange != MOA_XCHG_NCCL) {
-        delete pl;
-        return fail(MOA_ERR_INVALID_ARG, "the low-end breakpoint runs with the NCCL exchange (or EMULATED ranks)");
     }
     pl->chunks = 1;
 
@@ -771,13 +783,20 @@ int make_plan(int64_t n, int p, int sign, const moa_fft_options *opt, moa_fft_pl
         free_plan(pl);
         return fail(MOA_ERR_CUDA, "twiddle upload failed: %s", cudaGetErrorString(ce));
     }
-    static bool prepared = false;
-    if (!prepared) {
-        if ((ce = prepare_pass_kernels()) != cudaSuccess) {
-            free_plan(pl);
-            return fail(MOA_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(ce));
+    {
+        // the dynamic shared-memory limits are per-device function attributes: raise them
+        // once for every device a plan is built on (serialised across threads)
+        static std::mutex mu;
+        static uint64_t prepared_mask = 0;
+        std::lock_guard<std::mutex> lock(mu);
+        const uint64_t bit = 1ull << (pl->device & 63);
+        if (!(prepared_mask & bit)) {
+            if ((ce = prepare_pass_kernels()) != cudaSuccess) {
+                free_plan(pl);
+                return fail(MOA_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(ce));
+            }
+            prepared_mask |= bit;
         }
-        prepared = true;
     }
 
     // ---- buffers and passes

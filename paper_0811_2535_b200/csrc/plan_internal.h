@@ -16,6 +16,7 @@ namespace moa {
 int fail(int code, const char *fmt, ...);
 void clear_error();
 const char *last_error();
+int last_error_code();
 
 #define CUDA_TRY(expr)                                                                     \
     do {                                                                                   \
@@ -39,7 +40,15 @@ inline int ilog2(int64_t v) {
     return r;
 }
 inline bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+// Plan-time tuning knobs (MOA_FFT_*) for ablations and tuning sweeps.  They are read
+// ONLY when MOA_FFT_ABLATION=1 is set, so a stray environment variable cannot change
+// the product kernels or tile shapes; otherwise every knob takes its default.
+inline bool ablation_enabled() {
+    const char *s = getenv("MOA_FFT_ABLATION");
+    return s && *s && atoi(s) != 0;
+}
 inline int env_int(const char *name, int dflt) {
+    if (!ablation_enabled()) return dflt;
     const char *s = getenv(name);
     return (s && *s) ? atoi(s) : dflt;
 }

@@ -60,10 +60,38 @@ def test_plan_validation_errors(n, p, sign, code, needle):
     assert not h
     msg = lib.moa_fft_last_error().decode()
     assert needle in msg, msg
+    assert lib.moa_fft_last_error_code() == code   # the code that goes with the message
     with pytest.raises(moa.MoaError) as e:
         moa.Plan(n, p, sign)
-    assert e.value.code == -9  # Plan() wraps NULL as INVALID_ARG but keeps the message
+    assert e.value.code == code   # Plan() raises the library's own MOA_ERR_* code
     assert needle in str(e.value)
+
+
+def test_last_error_code_tracks_the_last_failure():
+    lib = moa.load()
+    assert not lib.moa_fft_plan(6, 1, -1)
+    assert lib.moa_fft_last_error_code() == -1          # INVALID_N (Fig 2.1: n = 2^t)
+    assert not lib.moa_fft_plan(16, 1, 2)
+    assert lib.moa_fft_last_error_code() == -3          # INVALID_SIGN
+    assert lib.moa_fft_execute(None, None, None) == -9
+    assert lib.moa_fft_last_error_code() == -9          # INVALID_ARG (NULL plan)
+
+
+def test_product_library_holds_only_adopted_kernels():
+    """The variants measured slower (persistent / TMA-staged / prefetching
+    passes, the L2-fused pass pair) are compiled only into libmoa_fft_variants.so."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not on PATH")
+    out = subprocess.run(["cuobjdump", "-sass", moa.lib_path()], capture_output=True, text=True)
+    assert out.returncode == 0
+    names = re.findall(r"Function : (\S+)", out.stdout)
+    assert names
+    banned = ("fft_pass_tma_kernel", "fft_pass_tpf_kernel", "fft_pass_pf_kernel", "fft_pass_rdb_kernel",
+              "fft_pass_persist_kernel", "fused_kernel", "fused_ticket_kernel")
+    bad = [nm for nm in names if any(b in nm for b in banned)]
+    assert not bad, bad[:5]
 
 
 def test_execute_rejects_null_plan():
