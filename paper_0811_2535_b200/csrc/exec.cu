@@ -60,12 +60,18 @@ int launch_pp(moa_fft_plan_s *pl, PassPlan &pp, int idx, const double2 *src, dou
     }
     char name[64];
     snprintf(name, sizeof name, "pass%d fft_pass%s<F=%d,T=%d>%s", idx,
-             pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : (pp.tmast && !peers ? "_tmast" : "")),
+             pp.big && !peers ? "_big" : (pp.tma ? "_tma" : (pp.pf_grid ? "_pf" : (pp.tmast && !peers ? "_tmast" : ""))),
              1 << pp.logF, pp.T,
              peers ? "+push" : "");
     ProfScope ps_(pl, name, 32 * pl->M * pl->batch);
     cudaError_t e;
-    if (pp.tma && !peers) {
+    if (pp.big && !peers) {
+        if (!D.last && pp.map_base != (const void *)src) {
+            int rc = encode_pass_map(pp, src);
+            if (rc) return rc;
+        }
+        e = launch_big(D, pp.map, pp.tiles, pl->stream);
+    } else if (pp.tma && !peers) {
         if (pp.map_base != (const void *)src) {
             int rc = encode_pass_map(pp, src);
             if (rc) return rc;

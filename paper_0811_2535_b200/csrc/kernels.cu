@@ -157,6 +157,9 @@ cudaError_t launch_fused(int, int, int, int, const FusedDesc &, const CUtensorMa
     return cudaErrorInvalidValue;
 }
 int fused_grid(int, int, int, int) { return 0; }
+int big_supported(int, int) { return 0; }
+cudaError_t prepare_big_kernels() { return cudaSuccess; }
+cudaError_t launch_big(const PassDesc &, const CUtensorMap &, int64_t, cudaStream_t) { return cudaErrorInvalidValue; }
 #endif
 
 cudaError_t prepare_pass_kernels() {
@@ -168,7 +171,7 @@ cudaError_t prepare_pass_kernels() {
         cudaError_t e = f();
         if (e != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    return prepare_big_kernels();
 }
 
 // ------------------------------------------------------------------ K1: bit reversal

@@ -90,6 +90,10 @@ struct FusedDesc {
 
 // host-side launchers (kernels.cu / fft_inst.cu)
 int sm_count();   // SM count of the current device (cached per device)
+// the persistent TMA-fed 4096-point pass (bigpass.cu): T = 2 tiles, one CTA per SM
+int big_supported(int logF, int T);
+cudaError_t prepare_big_kernels();
+cudaError_t launch_big(const PassDesc &d, const CUtensorMap &map, int64_t tiles, cudaStream_t s);
 int pass_supported(int logF, int T);
 size_t pass_smem_bytes(int logF, int T);
 int pass_threads(int logF, int T);

@@ -99,7 +99,7 @@ int encode_pass_map(PassPlan &pp, const void *base) {
     cuuint64_t dims[4], strides[3];
     cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
     cuuint32_t rank;
-    if (pp.tma == 1 || pp.tma == 4) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
+    if (pp.tma == 1 || pp.tma == 4 || (pp.big && !pp.d.last)) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
         const uint64_t B = (uint64_t)D.in_f, A = (uint64_t)D.V;
         rank = 3;
         dims[0] = 2 * B;
@@ -461,6 +461,14 @@ int build_passes(const moa_fft_plan_s *pl, int rank, int P, std::vector<PassPlan
         D.lV = ilog2(D.V);
         if (!pass_supported(pp.logF, pp.T))
             return fail(MOA_ERR_INVALID_ARG, "no pass kernel for F=2^%d T=%d", pp.logF, pp.T);
+        // ablation (libmoa_fft_variants.so, MOA_FFT_BIG=1): 4096-point passes of T = 2 as the
+        // persistent TMA-fed kernel (bigpass.cu) -- single-GPU, unbatched plans whose column
+        // tiles are plain [A][F][B] views and whose row tiles are contiguous rows.  Measured
+        // slower than three 256-point passes at 2^24, so never the default.
+        if (P == 1 && pl->batch == 1 && big_supported(pp.logF, pp.T) && pp.tiles >= 2 &&
+            env_int("MOA_FFT_BIG", 0) && D.in_shift == 0 && D.out_shift == 0 && D.pack_lp < 0 &&
+            (D.last ? D.in_f == 1 : (D.in_t == 1 && D.in_w == 0 && D.in_u == pp.T)))
+            pp.big = 1;
         out.push_back(pp);
     }
     return MOA_OK;

@@ -63,6 +63,7 @@ struct PassPlan {
     int tma_grid = 0;
     int pf_grid = 0;   // > 0: prefetching persistent kernel (fft_pass_pf_kernel)
     int tmast = 0;     // last pass stores through the TMA engine (launch_pass_tmast)
+    int big = 0;       // 4096-point pass as the persistent TMA-fed kernel (bigpass.cu)
     CUtensorMap omap;  // its output map (encoded for omap_base)
     const void *omap_base = nullptr;
     int io = 0;        // r-D axis passes: 0 = out -> out (in place), 1 = out -> work, 2 = work -> out

@@ -218,10 +218,10 @@ env = json.loads(sys.argv[1])
 for k, v in env.items():
     os.environ[k] = v
 worst = 0.0
-for t in (20, 22, 24):
+for t, lift in ((20, None), (22, None), (24, None), (24, [4096, 4096])):
     x = moa_inputs.signal_for(t)
     ref = oracle.fft(x, -1, threads=8)
-    plan = moa.Plan(1 << t)
+    plan = moa.Plan(1 << t, lift=lift)
     xd = torch.from_numpy(x).cuda()
     for _ in range(3):   # the fused kernel's counters are monotone across executes
         got = plan.execute(xd).cpu().numpy()
@@ -234,7 +234,7 @@ print("variant-ok", moa.lib_path(), worst)
 
 @pytest.mark.parametrize("env", [{"MOA_FFT_FUSE": "1"}, {"MOA_FFT_FUSE": "2"}, {"MOA_FFT_FUSE": "3"},
                                  {"MOA_FFT_PF": "1"}, {"MOA_FFT_PF": "3"}, {"MOA_FFT_TMA": "1"}, {"MOA_FFT_TMA": "2"},
-                                 {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}])
+                                 {"MOA_FFT_TMA": "1", "MOA_FFT_FUSE": "1"}, {"MOA_FFT_BIG": "1"}])
 def test_variant_kernels_parity(env):
     """The measured-and-not-adopted variants (L2-fused last passes, TMA-staged and
     prefetching persistent passes) live only in the ablation library
