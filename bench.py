@@ -316,7 +316,10 @@ def run_ours(args, rank: int, world: int):
     traffic = ncu_traffic(dom["name"], n, world)
     roofline = {"bound": "hbm", "kernel": dom["name"], "achieved": round(achieved, 1),
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                "traffic": traffic, "peak_source": peaks["source"],
+                "traffic": traffic,
+                "traffic_source": ("committed ncu --set full capture of this kernel (profiles/ncu_traffic.json), "
+                                   "not measured in this run") if traffic is not None else None,
+                "peak_source": peaks["source"],
                 "share_of_step": round(dom["avg_us"] * dom["launches"] / max(kernel_total, 1e-9), 3),
                 "kernel_timing": "per-kernel CUDA events on the plan stream over a second run of the same K "
                                  "steps (events between launches; the headline timed region has none)"}
@@ -353,6 +356,16 @@ def run_ours(args, rank: int, world: int):
                "h2d_bytes_per_step": int(hin.numel() * 16), "d2h_bytes_per_step": int(hout.numel() * 16),
                "steps": e_steps, "ms_per_step": round(e_el / e_steps * 1e3, 3)}
 
+    # ---- p > 1: no-overlap diagnostic of the exchange: the unchunked NCCL
+    # plan (all-to-all on the plan stream, between the phase-1 passes and the combine)
+    # with an event pair around every launch
+    a2a = None
+    if world > 1:
+        try:
+            a2a = a2a_diagnostic(moa, n, world, stream, x, args.steps, kstats, elapsed / args.steps, dev)
+        except Exception as e:  # noqa: BLE001 - diagnostics never kill the bench line
+            a2a = {"error": str(e)[:200]}
+
     if rank == 0:
         cpu = None
         if not args.no_cpu:
@@ -360,35 +373,111 @@ def run_ours(args, rank: int, world: int):
             cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{args.cpu_reps} full n=2^{t} oracle transforms ({dt:.2f} s each)",
                    "cpu": cpu_model()}
+        step_s = elapsed / args.steps
+        # SURVEY §8(d) algorithmic bytes: 32 n ceil(t/13) on one GPU (d(n) passes of <= 2^13
+        # points); 32 M (d(M) + 1) per rank for p > 1 (the local passes + the P-point combine)
+        M = n // world
+        tm = M.bit_length() - 1
+        survey_bytes = 32 * n * -(-t // 13) if world == 1 else 32 * M * (-(-tm // 13) + 1)
+        hbm = {"alg_bytes_survey": int(survey_bytes),
+               "alg_GBps_survey": round(survey_bytes / step_s / 1e9, 1),
+               "frac_survey": round(survey_bytes / step_s / 1e9 / peaks["hbm_gbs"], 4),
+               "survey_rule": "32 n ceil(t/13) (p = 1) / 32 (n/p)(d(n/p) + 1) per rank: the bytes of the "
+                              "fewest <= 2^13-point passes (SURVEY §8(d)); the headline fraction",
+               "alg_bytes_plan": int(info["hbm_bytes"]),
+               "alg_GBps_plan": round(info["hbm_bytes"] / step_s / 1e9, 1),
+               "frac_plan": round(info["hbm_bytes"] / step_s / 1e9 / peaks["hbm_gbs"], 4),
+               "plan_rule": f"32 n x {info['passes']} passes of this plan's lifting {info['lift']} (its own "
+                            "traffic; higher than the survey's when the plan makes more passes)",
+               "peak_GBps": peaks["hbm_gbs"], "peak_source": peaks["source"]}
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
+                "gpus_active": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_block(t, world, info, args.exchange),
-                "hbm": {"alg_bytes_per_step": int(info["hbm_bytes"]),
-                        "alg_GBps": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9, 1),
-                        "frac_of_measured": round(info["hbm_bytes"] / (elapsed / args.steps) / 1e9
-                                                  / peaks["hbm_gbs"], 4)},
+                "hbm": hbm,
                 "roofline": roofline, "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e,
                 "plan_ms": round(plan_ms, 2), "step_ms": step_stats,
                 "gpu_launches": int(args.steps * info["launches"]),
                 "clocks": sampler.summary()}
-        if world > 1:
-            a2a = [k for k in kstats if "NCCL" in k["name"]]
-            if a2a:
-                bw = a2a[0]["alg_bytes"] / (a2a[0]["avg_us"] * 1e-6) / 1e9
-                line["a2a"] = {"GBps_per_rank": round(bw, 1), "frac_of_770": round(bw / 770.0, 4),
-                               "avg_us": round(a2a[0]["avg_us"], 2)}
+        if a2a is not None:
+            line["a2a"] = a2a
         print(json.dumps(line), flush=True)
     plan.destroy()
     if world > 1:
         moa.dist_finalize()
 
 
+def a2a_diagnostic(moa, n, world, stream, x, steps, kstats_main, step_s, dev):
+    """Exchange cost without overlap (p > 1), max over ranks:
+    t_a2a  = the NCCL send/recv group of the unchunked NCCL plan (events on the plan stream);
+    algBw  = 16 M / t_a2a (this rank's buffer), busBw = algBw (p-1)/p (bytes that cross
+             NVLink), as fractions of 900 GB/s nominal and 770 GB/s measured peer copy;
+    fused  = for the P2P plan, the push pass minus the same pass storing locally (the
+             NCCL plan's last pass): the exchange time the fused kernel adds;
+    overlap efficiency = (t_p1 + t_a2a + t_p2 - t_step) / min(t_a2a, t_p1 + t_p2)."""
+    import torch
+    import torch.distributed as dist
+    M = n // world
+    diag = moa.Plan(n, world, -1, stream=stream, chunks=1)
+    out = torch.empty_like(x)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            diag.execute(x, out)
+    diag.set_profiling(True)
+    diag.get_profile()
+    dist.barrier()
+    with torch.cuda.stream(stream):
+        for _ in range(steps):
+            diag.execute(x, out)
+    prof = diag.get_profile()
+    diag.set_profiling(False)
+    torch.cuda.synchronize()
+    diag.destroy()
+    t_a2a = sum(k["avg_us"] for k in prof if "NCCL" in k["name"]) * 1e-6
+    t_comb = sum(k["avg_us"] for k in prof if "pcombine" in k["name"]) * 1e-6
+    t_p1 = sum(k["avg_us"] for k in prof if k["name"].startswith("pass")) * 1e-6
+    last_local = max((k for k in prof if k["name"].startswith("pass")), key=lambda k: k["name"])["avg_us"] * 1e-6
+    push = [k for k in kstats_main if "+push" in k["name"]]
+    t_push_extra = (push[0]["avg_us"] * 1e-6 - last_local) if push else None
+    vals = torch.tensor([t_a2a, t_p1, t_comb, t_push_extra if t_push_extra is not None else -1.0],
+                        dtype=torch.float64, device=dev)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_a2a, t_p1, t_comb, t_push_extra = [float(v) for v in vals.tolist()]
+    alg = 16.0 * M / t_a2a / 1e9 if t_a2a > 0 else None
+    bus = alg * (world - 1) / world if alg else None
+    res = {"t_a2a_us": round(t_a2a * 1e6, 2), "t_phase1_us": round(t_p1 * 1e6, 2),
+           "t_combine_us": round(t_comb * 1e6, 2), "bytes_sent_per_rank": int(16 * M // world * (world - 1)),
+           "algBw_GBps": round(alg, 1) if alg else None, "busBw_GBps": round(bus, 1) if bus else None,
+           "busBw_frac_of_900": round(bus / 900.0, 4) if bus else None,
+           "busBw_frac_of_770_measured": round(bus / 770.0, 4) if bus else None,
+           "overlap_efficiency": round((t_p1 + t_a2a + t_comb - step_s) / min(t_a2a, t_p1 + t_comb), 4)
+           if t_a2a > 0 else None,
+           "how": "unchunked NCCL plan, events around every launch on the plan stream, max over ranks"}
+    if t_push_extra is not None and t_push_extra > -1.0:
+        res["fused_push_extra_us"] = round(t_push_extra * 1e6, 2)
+        sent = 16.0 * M * (world - 1) / world
+        if t_push_extra > 0:
+            res["fused_push_GBps"] = round(sent / t_push_extra / 1e9, 1)
+    return res
+
+
 class moa_stat(__import__("ctypes").Structure):
     import ctypes as _c
     _fields_ = [("name", _c.c_char * 64), ("launches", _c.c_int), ("total_ms", _c.c_double),
                 ("alg_bytes", _c.c_int64)]
+
+
+def self_launch(n: int) -> int:
+    """Re-run this command as n ranks: python -m torch.distributed.run --nproc-per-node n."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -409,8 +498,16 @@ def main():
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` without a launcher: start N ranks (one process per GPU) under
+        # torch.distributed.run on this node and relay rank 0's line
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

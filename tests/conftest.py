@@ -6,6 +6,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+TESTS = os.path.dirname(os.path.abspath(__file__))
+if TESTS not in sys.path:
+    sys.path.insert(0, TESTS)
 
 
 def pytest_configure(config):
@@ -35,3 +38,26 @@ def parse_complex_list(s):
         re_, im_ = tok.split(",")
         out.append(complex(float(re_), float(im_)))
     return out
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Print the achieved relL2 of every recorded GPU parity check against its bar."""
+    try:
+        import _parity
+    except Exception:
+        return
+    recs = _parity.RECORDS
+    if not recs:
+        return
+    tr = terminalreporter
+    tr.section("achieved relL2 (GPU vs oracle; bar = 1e-12 log2 n)")
+    worst = {}
+    for r in recs:
+        k = (r["test"], r["t"])
+        if k not in worst or r["relL2"] > worst[k]["relL2"]:
+            worst[k] = r
+    for (name, t), r in sorted(worst.items(), key=lambda kv: (kv[0][1], kv[0][0])):
+        tr.write_line(f"t={t:2d}  relL2={r['relL2']:.3e}  bar={r['bar']:.1e}  margin={r['bar'] / max(r['relL2'], 1e-300):9.0f}x  {name}")
+    out = os.environ.get("MOA_PARITY_LOG")
+    if out:
+        _parity.dump(out)

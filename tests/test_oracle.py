@@ -386,3 +386,32 @@ def test_fftn_matches_fft2_and_numpy():
     assert oracle.rel_l2(oracle.fftn(x), np.fft.fftn(x)) <= 1e-14
     y = x.reshape(16, 256)
     assert np.array_equal(oracle.fftn(y), oracle.fft2(y))
+
+
+def test_rel_l2_closed_forms_pin_the_checker():
+    """The parity metric itself (oracle.rel_l2) against closed forms,
+    so a broken checker cannot pass a wrong GPU result: one perturbed element gives
+    |d| / ||x||, a swapped pair sqrt(2) |x_a - x_b| / ||x||, a scaled vector |a - 1|, a zero
+    reference ||g||; and at the GPU bar (1e-12 log2 n) a perturbation of 1e-10 ||x|| fails."""
+    rng = np.random.default_rng(7)
+    n = 4096
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    nx = np.sqrt(np.sum(np.abs(x) ** 2))
+    d = 3e-7 - 4e-7j
+    y = x.copy()
+    y[1234] += d
+    assert abs(oracle.rel_l2(y, x) - abs(d) / nx) <= 1e-9 * abs(d) / nx
+    s = x.copy()
+    s[[5, 3000]] = x[[3000, 5]]
+    want = np.sqrt(2) * abs(x[5] - x[3000]) / nx
+    assert abs(oracle.rel_l2(s, x) - want) <= 1e-12 * want
+    assert abs(oracle.rel_l2(1.5 * x, x) - 0.5) <= 1e-15
+    assert oracle.rel_l2(x, x) == 0.0
+    assert abs(oracle.rel_l2(x, np.zeros(n, dtype=np.complex128)) - nx) <= 1e-12 * nx
+    z = x.copy()
+    z[17] += 1e-10 * nx
+    assert oracle.rel_l2(z, x) > 1e-12 * 12          # fails the bar at n = 2^12
+    # l2_parts over chunks equals the whole sum (the chunked form the large tests use)
+    a, b = oracle.l2_parts(y, x, chunk=1000)
+    a2, b2 = oracle.l2_parts(y, x)
+    assert abs(a - a2) <= 1e-20 and abs(b - b2) <= 1e-9
