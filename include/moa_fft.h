@@ -309,6 +309,48 @@ int moa_dist_init(int rank, int p, const void *id_128B);
 int moa_dist_finalize(void);
 
 /*
+ * Redistributions between the paper's layouts of a distributed n-vector (SURVEY §8(f)
+ * N2; Figs 5.2-5.5, 5.8, 5.9).  psize = n/p.
+ *   MOA_LAYOUT_BLOCK   rank r holds x[r*psize + i], i < psize             (xblock)
+ *   MOA_LAYOUT_CYCLIC  rank r holds x[r + p*j],     j < psize             (xcyclic, P:799,
+ *                      the transform's own in/out layout for p > 1)
+ *   MOA_LAYOUT_CENTRAL rank 0 holds all n elements in natural order, the other ranks
+ *                      none (the paper's processor 0)
+ *   route MOA_ROUTE_DIRECT:  one point-to-point round in which every rank sends each
+ *                      other rank its part directly (Fig 5.3 / Fig 5.9, P:828-842,
+ *                      m(m-1) messages of psize/m for block <-> cyclic,
+ *                      P:1043); CENTRAL <-> anything is a scatter / gather (m-1 messages)
+ *   route MOA_ROUTE_CENTRAL: block <-> cyclic through processor 0 (Fig 5.4, P:844,
+ *                      P:848-874): gather, then scatter -- 2(m-1) messages, every
+ *                      element moved twice, processor 0's links the bottleneck
+ * The local permutations (the pack of the strided SEND sections and the unpack of the
+ * received ones) are CUDA kernels; the transfers are NCCL send/recv groups over the
+ * library's communicator (moa_dist_init; collective: every rank calls execute in the
+ * same order), or device copies when mode == MOA_MODE_EMULATED (all p ranks' buffers
+ * back to back on this GPU: BLOCK / CYCLIC buffers hold p*psize elements, rank r's at
+ * offset r*psize; CENTRAL buffers hold n elements) or p == 1.
+ *   moa_redist_plan: n = 2^t (1 <= t <= 32), p a power of two <= 16 with psize >= p,
+ *     from/to MOA_LAYOUT_*, route MOA_ROUTE_*, mode MOA_MODE_LIFTED (real ranks) or
+ *     MOA_MODE_EMULATED.  Owns its scratch (psize elements per rank for the direct block
+ *     <-> cyclic routes, n on rank 0 for the central ones).  NULL on error.
+ *   moa_redist_execute: in / out device pointers in the layouts above, out of place
+ *     (in != out); a rank that holds no elements of a layout may pass NULL for it.
+ *     Asynchronous on the plan's stream.  MOA_OK / MOA_ERR_ALIGN / MOA_ERR_INVALID_ARG /
+ *     MOA_ERR_CUDA / MOA_ERR_NCCL.
+ *   moa_redist_info: messages between distinct ranks per execute (whole job), the largest
+ *     number of bytes any one rank sends, and this rank's element counts in and out.
+ */
+enum { MOA_LAYOUT_BLOCK = 0, MOA_LAYOUT_CYCLIC = 1, MOA_LAYOUT_CENTRAL = 2 };
+enum { MOA_ROUTE_DIRECT = 0, MOA_ROUTE_CENTRAL = 1 };
+typedef struct moa_redist_s *moa_redist_t;
+moa_redist_t moa_redist_plan(int64_t n, int p, int from, int to, int route, int mode);
+int moa_redist_execute(moa_redist_t plan, const void *in, void *out);
+int moa_redist_set_stream(moa_redist_t plan, void *stream);
+int moa_redist_info(moa_redist_t plan, int64_t *messages, int64_t *max_rank_bytes, int64_t *elems_in,
+                    int64_t *elems_out);
+void moa_redist_destroy(moa_redist_t plan);
+
+/*
  * Test/bench helper (not part of the transform): fill `count` complex128 values
  * at device pointer out with x_g = u(seed, 2g) + i*u(seed, 2g+1),
  * g = first + stride*i, u = SplitMix64 mapped to [-1, 1) (the recipe of

@@ -18,6 +18,8 @@ import os
 from . import build as _build
 
 __all__ = ["Plan", "Plan2D", "PlanND", "fft2", "fftn", "fft", "dist_fft", "scatter_cyclic", "gather_cyclic", "ifft_unnormalized", "gen_uniform", "dist_init", "dist_finalize", "describe_pass",
+           "Redist", "block_to_cyclic", "cyclic_to_block", "block_to_cyclic_via_central", "dist_fft_block",
+           "LAYOUT_BLOCK", "LAYOUT_CYCLIC", "LAYOUT_CENTRAL", "ROUTE_DIRECT", "ROUTE_CENTRAL",
            "MoaError", "MODE_LIFTED", "MODE_LITERAL", "MODE_EMULATED", "XCHG_NCCL", "XCHG_P2P",
            "XCHG_P2P_EXTERNAL", "lib_path", "load"]
 
@@ -57,7 +59,8 @@ EXPORTS = ["moa_fft_plan", "moa_fft_plan_ex", "moa_fft_execute", "moa_fft_execut
            "moa_dist_unique_id", "moa_dist_init", "moa_dist_finalize", "moa_gen_uniform",
            "moa_fft_version", "moa_fft_set_profiling", "moa_fft_get_profile", "moa_fft_describe_pass",
            "moa_fft_ipc_handle", "moa_fft_ipc_open", "moa_fft_enable_p2p", "moa_fft_execute_phase",
-           "moa_fft_plan_2d", "moa_fft_plan_nd", "moa_fft_default_lifting", "moa_fft_last_error_code"]
+           "moa_fft_plan_2d", "moa_fft_plan_nd", "moa_fft_default_lifting", "moa_fft_last_error_code",
+           "moa_redist_plan", "moa_redist_execute", "moa_redist_set_stream", "moa_redist_info", "moa_redist_destroy"]
 
 _lib = None
 
@@ -103,6 +106,13 @@ def load(build_if_needed: bool = True):
     lib.moa_dist_unique_id.argtypes = [vp]
     lib.moa_dist_init.argtypes = [ci, ci, vp]
     lib.moa_gen_uniform.argtypes = [ctypes.c_uint64, i64, i64, i64, vp, vp]
+    lib.moa_redist_plan.argtypes = [i64, ci, ci, ci, ci, ci]
+    lib.moa_redist_plan.restype = vp
+    lib.moa_redist_execute.argtypes = [vp, vp, vp]
+    lib.moa_redist_set_stream.argtypes = [vp, vp]
+    lib.moa_redist_info.argtypes = [vp, vp, vp, vp, vp]
+    lib.moa_redist_destroy.argtypes = [vp]
+    lib.moa_redist_destroy.restype = None
     lib.moa_fft_version.restype = ctypes.c_char_p
     lib.moa_fft_set_profiling.argtypes = [vp, ci]
     lib.moa_fft_get_profile.argtypes = [vp, vp, ci]
@@ -461,94 +471,114 @@ def dist_fft(x_local, n: int, sign: int = -1, out=None, exchange: int = XCHG_NCC
         plan.destroy()
 
 
-def scatter_cyclic(x0, n: int, group=None, device=None):
+LAYOUT_BLOCK, LAYOUT_CYCLIC, LAYOUT_CENTRAL = 0, 1, 2
+ROUTE_DIRECT, ROUTE_CENTRAL = 0, 1
+
+
+class Redist:
+    """A redistribution between the paper's layouts of a distributed n-vector
+    (moa_redist_plan, include/moa_fft.h): LAYOUT_BLOCK (rank r holds
+    x[r*psize:(r+1)*psize]), LAYOUT_CYCLIC (x[r::p], the transform's layout) and
+    LAYOUT_CENTRAL (all of x on rank 0).  route ROUTE_DIRECT = Fig 5.3/5.9 (one round,
+    m(m-1) messages), ROUTE_CENTRAL = Fig 5.4 (gather to processor 0, scatter back).
+    mode MODE_LIFTED = real ranks over the library's NCCL communicator (dist_init first),
+    MODE_EMULATED = the p ranks' buffers back to back on this GPU."""
+
+    def __init__(self, n: int, p: int, frm: int, to: int, route: int = ROUTE_DIRECT, mode: int = MODE_LIFTED,
+                 stream=None):
+        lib = load()
+        h = lib.moa_redist_plan(int(n), int(p), int(frm), int(to), int(route), int(mode))
+        if not h:
+            _plan_err(lib)
+        self._h = h
+        self.n, self.p, self.frm, self.to, self.route, self.mode = int(n), int(p), int(frm), int(to), int(route), mode
+        s = _cur_stream() if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
+        rc = lib.moa_redist_set_stream(h, s)
+        if rc:
+            _err(rc)
+
+    def info(self) -> dict:
+        m, b, ei, eo = (ctypes.c_int64() for _ in range(4))
+        rc = _lib.moa_redist_info(self._h, ctypes.byref(m), ctypes.byref(b), ctypes.byref(ei), ctypes.byref(eo))
+        if rc:
+            _err(rc)
+        return {"messages": m.value, "max_rank_bytes": b.value, "elems_in": ei.value, "elems_out": eo.value}
+
+    def execute(self, x, out=None):
+        """x: this rank's elements (complex128 CUDA tensor, or None where the layout gives
+        the rank none); returns out (allocated when None)."""
+        import torch
+        inf = self.info()
+        if out is None and inf["elems_out"] > 0:
+            dev = x.device if x is not None else torch.device("cuda", torch.cuda.current_device())
+            out = torch.empty(inf["elems_out"], dtype=torch.complex128, device=dev)
+        for v, k, what in ((x, "elems_in", "x"), (out, "elems_out", "out")):
+            if v is not None and (v.dtype != torch.complex128 or not v.is_cuda or not v.is_contiguous()
+                                  or v.numel() != inf[k]):
+                raise ValueError(f"{what} must be a contiguous complex128 CUDA tensor of {inf[k]} elements")
+        rc = _lib.moa_redist_execute(self._h, _ptr(x) if x is not None else None,
+                                     _ptr(out) if out is not None else None)
+        if rc:
+            _err(rc)
+        return out
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            _lib.moa_redist_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def _redist(x, n: int, frm: int, to: int, route: int = ROUTE_DIRECT):
+    """One redistribution over the library's communicator (collective; dist_init first)."""
+    import torch
+    import torch.distributed as dist
+    plan = Redist(n, dist.get_world_size(), frm, to, route)
+    try:
+        return plan.execute(x)
+    finally:
+        torch.cuda.current_stream().synchronize()
+        plan.destroy()
+
+
+def scatter_cyclic(x0, n: int):
     """The paper's DISTRIBUTE_CENTRALIZED_TO_CYCLIC_PARTITIONED (Fig 5.8):
-    rank 0 holds the whole x0 (n elements); rank r receives xcyclic = x0[r::p] (psize
-    elements).  Layout plumbing outside the transform (torch.distributed scatter);
-    `device` is where the local slice lives (default: x0's device on rank 0, CPU
-    elsewhere unless given)."""
-    import torch
+    rank 0 holds x0 (n elements, CUDA), rank r receives x0[r::p].  Library pack kernel +
+    NCCL scatter; other ranks pass None."""
+    return _redist(x0, n, LAYOUT_CENTRAL, LAYOUT_CYCLIC)
+
+
+def gather_cyclic(xcyclic, n: int):
+    """DISTRIBUTE_CYCLIC_PARTITIONED_TO_CENTRALIZED (Fig 5.8): rank r holds
+    X[r::p]; rank 0 returns the whole n-vector in natural order, the others None."""
+    return _redist(xcyclic, n, LAYOUT_CYCLIC, LAYOUT_CENTRAL)
+
+
+def block_to_cyclic(x_block, n: int = None, route: int = ROUTE_DIRECT):
+    """Natural block x[r*psize:(r+1)*psize] -> x[r::p]: Fig 5.3/5.9's direct exchange
+    (route ROUTE_DIRECT) or Fig 5.4 through processor 0 (ROUTE_CENTRAL)."""
     import torch.distributed as dist
-    rank, p = dist.get_rank(group), dist.get_world_size(group)
-    psize = n // p
-    dev = device if device is not None else (x0.device if rank == 0 else torch.device("cpu"))
-    mine = torch.empty(psize, dtype=torch.complex128, device=dev)
-    chunks = None
-    if rank == 0:
-        chunks = [x0[r::p].contiguous().view(torch.float64).to(dev) for r in range(p)]
-    out = mine.view(torch.float64)
-    dist.scatter(out, chunks, src=0, group=group)
-    return mine
+    n = n or x_block.numel() * dist.get_world_size()
+    return _redist(x_block, n, LAYOUT_BLOCK, LAYOUT_CYCLIC, route)
 
 
-def gather_cyclic(xcyclic, n: int, group=None):
-    """The paper's DISTRIBUTE_CYCLIC_PARTITIONED_TO_CENTRALIZED (Fig 5.8):
-    rank r holds X[r::p]; rank 0 returns the whole n-vector in natural order (x0(r:n-1:m)
-    = xcyclic of rank r), the other ranks return None."""
-    import torch
+def cyclic_to_block(x_cyclic, n: int = None, route: int = ROUTE_DIRECT):
+    """x[r::p] -> the natural block x[r*psize:(r+1)*psize] (the transform's output to
+    block-natural order)."""
     import torch.distributed as dist
-    rank, p = dist.get_rank(group), dist.get_world_size(group)
-    psize = n // p
-    flat = xcyclic.contiguous().view(torch.float64)
-    parts = [torch.empty_like(flat) for _ in range(p)] if rank == 0 else None
-    dist.gather(flat, parts, dst=0, group=group)
-    if rank != 0:
-        return None
-    x0 = torch.empty(n, dtype=torch.complex128, device=xcyclic.device)
-    for r in range(p):
-        x0[r::p] = parts[r].view(torch.complex128)[:psize]
-    return x0
+    n = n or x_cyclic.numel() * dist.get_world_size()
+    return _redist(x_cyclic, n, LAYOUT_CYCLIC, LAYOUT_BLOCK, route)
 
 
-def block_to_cyclic(x_block, group=None):
-    """Fig 5.3 / Fig 5.9's direct redistribution applied to the INPUT: rank r
-    holds the natural block x[r*psize : (r+1)*psize] and gets xcyclic = x[r::p] -- one
-    all-to-all (m(m-1) messages of psize/m): element i of block r goes to rank i mod p,
-    slot r*psize/p + i div p.  Layout plumbing over torch.distributed, outside the
-    transform (block-natural in/out costs two extra all-to-alls)."""
-    import torch
-    import torch.distributed as dist
-    p = dist.get_world_size(group)
-    m = x_block.numel()
-    send = x_block.contiguous().view(m // p, p).t().contiguous()        # [dst][q]: x[r*psize + dst + p*q]
-    recv = torch.empty(2 * m, dtype=torch.float64, device=x_block.device)
-    dist.all_to_all_single(recv, send.view(torch.float64).reshape(-1), group=group)
-    return recv.view(torch.complex128)                                  # [src r][q] = x[rank + p*(r*psize/p + q)]
-
-
-def cyclic_to_block(x_cyclic, group=None):
-    """The inverse redistribution for the OUTPUT: rank d holds X[d + p*i'] (the transform's
-    xcyclic) and gets the natural block X[d*psize : (d+1)*psize] -- chunk r of the cyclic
-    slice (i' in [r*psize/p, (r+1)*psize/p)) goes to rank r, which interleaves the p
-    chunks it receives (element q of source d lands at d + p*q)."""
-    import torch
-    import torch.distributed as dist
-    p = dist.get_world_size(group)
-    m = x_cyclic.numel()
-    recv = torch.empty(2 * m, dtype=torch.float64, device=x_cyclic.device)
-    dist.all_to_all_single(recv, x_cyclic.contiguous().view(torch.float64), group=group)
-    return recv.view(torch.complex128).view(p, m // p).t().reshape(-1)
-
-
-def block_to_cyclic_via_central(x_block, group=None):
-    """Fig 5.4: the same redistribution routed through processor 0 --
-    every block is sent to rank 0 (m-1 messages of psize), which sends every rank its
-    cyclic slice (m-1 messages of psize): 2(m-1) messages, each element moved twice,
-    rank 0's links the bottleneck.  The ablation of Fig 5.9's direct exchange."""
-    import torch
-    import torch.distributed as dist
-    rank, p = dist.get_rank(group), dist.get_world_size(group)
-    m = x_block.numel()
-    flat = x_block.contiguous().view(torch.float64)
-    parts = [torch.empty_like(flat) for _ in range(p)] if rank == 0 else None
-    dist.gather(flat, parts, dst=0, group=group)                        # x0 on processor 0
-    mine = torch.empty(2 * m, dtype=torch.float64, device=x_block.device)
-    chunks = None
-    if rank == 0:
-        x0 = torch.cat([q.view(torch.complex128) for q in parts])
-        chunks = [x0[r::p].contiguous().view(torch.float64) for r in range(p)]
-    dist.scatter(mine, chunks, src=0, group=group)                      # xcyclic from processor 0
-    return mine.view(torch.complex128)
+def block_to_cyclic_via_central(x_block, n: int = None):
+    """Fig 5.4: the block -> cyclic redistribution routed through
+    processor 0 (2(m-1) messages, every element moved twice)."""
+    return block_to_cyclic(x_block, n, ROUTE_CENTRAL)
 
 
 def dist_fft_block(x_block, n: int, sign: int = -1, exchange: int = XCHG_NCCL, breakpoint: int = 0):
@@ -556,8 +586,8 @@ def dist_fft_block(x_block, n: int, sign: int = -1, exchange: int = XCHG_NCCL, b
     holds x[r*psize : (r+1)*psize] and returns X[r*psize : (r+1)*psize].  = block_to_cyclic
     -> dist_fft -> cyclic_to_block: the transform's own exchange plus two layout
     all-to-alls (torch.distributed; collective)."""
-    xc = block_to_cyclic(x_block)
-    return cyclic_to_block(dist_fft(xc, n, sign, exchange=exchange, breakpoint=breakpoint))
+    xc = block_to_cyclic(x_block, n)
+    return cyclic_to_block(dist_fft(xc, n, sign, exchange=exchange, breakpoint=breakpoint), n)
 
 
 def default_lifting(n: int, p: int = 1) -> list:

@@ -29,7 +29,7 @@ FLAGS = [*os.environ.get("MOA_NVCC_EXTRA", "").split(),
          "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"]
 
-SOURCES = ["kernels.cu", "plan.cu", "exec.cu", "abi.cu", "dist.cu"] + (["fused.cu", "bigpass.cu"] if VARIANTS else [])
+SOURCES = ["kernels.cu", "plan.cu", "exec.cu", "abi.cu", "dist.cu", "redist.cu"] + (["fused.cu", "bigpass.cu"] if VARIANTS else [])
 if VARIANTS:
     FLAGS.append("-DMOA_VARIANTS=1")
 INST_LOGF = list(range(1, 14))

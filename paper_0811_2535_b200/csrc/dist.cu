@@ -132,6 +132,52 @@ int dist_alltoall(const double2 *send, double2 *recv, int64_t chunk, int p, int 
     return MOA_OK;
 }
 
+// General point-to-point round (the N2 redistributions, redist.cu): this rank sends
+// send_n[d] elements from send[d] to every rank d and receives recv_n[s] elements into
+// recv[s] from every rank s, in one NCCL group; the self entry is a device copy.
+// Counts of 0 skip the pair (scatter / gather rounds touch only rank 0's pairs).
+int dist_sendrecv(const double2 *const *send, const int64_t *send_n, double2 *const *recv, const int64_t *recv_n,
+                  int p, int rank, cudaStream_t s, std::string *err) {
+    if (!g_comm) {
+        *err = "no communicator (moa_dist_init)";
+        return MOA_ERR_NO_DIST;
+    }
+    if (send_n[rank] != recv_n[rank]) {
+        *err = "self send and receive counts differ";
+        return MOA_ERR_INVALID_ARG;
+    }
+    if (send_n[rank] > 0) {
+        cudaError_t ce = cudaMemcpyAsync(recv[rank], send[rank], send_n[rank] * sizeof(double2),
+                                         cudaMemcpyDeviceToDevice, s);
+        if (ce != cudaSuccess) {
+            *err = std::string("self copy failed: ") + cudaGetErrorString(ce);
+            return MOA_ERR_CUDA;
+        }
+    }
+    ncclResult_t r = g_nccl.GroupStart();
+    if (r) {
+        *err = nccl_msg("ncclGroupStart", r);
+        return MOA_ERR_NCCL;
+    }
+    for (int o = 1; o < p; ++o) {
+        const int peer = (rank + o) % p, from = (rank - o + p) % p;
+        if (send_n[peer] > 0) r = g_nccl.Send(send[peer], (size_t)send_n[peer] * 2, kNcclFloat64, peer, g_comm, s);
+        if (!r && recv_n[from] > 0)
+            r = g_nccl.Recv(recv[from], (size_t)recv_n[from] * 2, kNcclFloat64, from, g_comm, s);
+        if (r) {
+            g_nccl.GroupEnd();
+            *err = nccl_msg("ncclSend/ncclRecv", r);
+            return MOA_ERR_NCCL;
+        }
+    }
+    r = g_nccl.GroupEnd();
+    if (r) {
+        *err = nccl_msg("ncclGroupEnd", r);
+        return MOA_ERR_NCCL;
+    }
+    return MOA_OK;
+}
+
 // Stream-ordered barrier of all ranks (the P2P exchange's only collective): an
 // 8-byte all-reduce completes on a rank only after every rank has enqueued it,
 // i.e. after every rank's preceding kernels (the fused push) have finished.

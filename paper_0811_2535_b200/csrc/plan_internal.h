@@ -31,6 +31,8 @@ int dist_world(int *rank, int *size);
 int dist_alltoall(const double2 *send, double2 *recv, int64_t chunk, int p, int rank, cudaStream_t s,
                   std::string *err);
 int dist_barrier(cudaStream_t s, std::string *err);
+int dist_sendrecv(const double2 *const *send, const int64_t *send_n, double2 *const *recv, const int64_t *recv_n,
+                  int p, int rank, cudaStream_t s, std::string *err);
 int dist_allgather_sync(const void *send_dev, void *recv_dev, size_t bytes, cudaStream_t s, std::string *err);
 
 // ------------------------------------------------------------------ small helpers

@@ -100,6 +100,7 @@ def test_bench_reference_arm_torchrun_two_ranks():
 
 def _layout_worker(rank, world, port, q):
     sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     try:
@@ -108,9 +109,10 @@ def _layout_worker(rank, world, port, q):
         import paper_0811_2535_b200 as moa
         n = 1 << 10
         x0 = torch.from_numpy(moa_inputs.signal_for(10)) if rank == 0 else None
-        mine = moa.scatter_cyclic(x0, n)
+        import _layouts_torch as lt
+        mine = lt.scatter_cyclic(x0, n)
         ok_scatter = np.array_equal(mine.numpy(), moa_inputs.signal_for(10)[rank::world])
-        back = moa.gather_cyclic(mine, n)
+        back = lt.gather_cyclic(mine, n)
         ok_gather = (rank != 0) or np.array_equal(back.numpy(), moa_inputs.signal_for(10))
         q.put((rank, bool(ok_scatter and ok_gather)))
         dist.destroy_process_group()
@@ -152,9 +154,10 @@ def _block_worker(rank, world, port, q):
         chunk = m // p
         x = moa_inputs.signal_for(t)
         xb = torch.from_numpy(x[rank * m:(rank + 1) * m].copy())
-        xc = moa.block_to_cyclic(xb)                                     # Fig 5.3 / 5.9 direct
+        import _layouts_torch as lt
+        xc = lt.block_to_cyclic(xb)                                      # Fig 5.3 / 5.9 direct
         ok_direct = np.array_equal(xc.numpy(), x[rank::p])
-        xv = moa.block_to_cyclic_via_central(xb)                         # Fig 5.4 via processor 0
+        xv = lt.block_to_cyclic_via_central(xb)                          # Fig 5.4 via processor 0
         ok_central = np.array_equal(xv.numpy(), x[rank::p])
         # the partitioned transform on the cyclic slice (product maps + a real exchange),
         # then the output back to natural blocks: X[r*psize : (r+1)*psize]
@@ -163,7 +166,7 @@ def _block_worker(rank, world, port, q):
         dist.all_to_all_single(recv, torch.from_numpy(send.view(np.float64).copy()),
                                [2 * chunk] * p, [2 * chunk] * p)
         Xc = torch.from_numpy(pcombine(recv.numpy().view(np.complex128), p).copy())
-        Xb = moa.cyclic_to_block(Xc)
+        Xb = lt.cyclic_to_block(Xc)
         ref = oracle.fft(x, -1)
         err = oracle.rel_l2(Xb.numpy(), ref[rank * m:(rank + 1) * m])
         q.put((rank, (ok_direct, ok_central, err)))
