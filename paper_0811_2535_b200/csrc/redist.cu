@@ -35,39 +35,58 @@
 
 namespace moa {
 
-// dst[d*q + j] = src[d + P*j]  (the [q][P] -> [P][q] transpose; P <= 16 values per thread,
-// loaded together so a warp reads 32*P consecutive elements)
-template <int P>
-__global__ void deinterleave_kernel(const double2 *__restrict__ src, double2 *__restrict__ dst, int64_t q) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < q; j += (int64_t)gridDim.x * blockDim.x) {
-        double2 v[P];
-#pragma unroll
-        for (int d = 0; d < P; ++d) v[d] = __ldg(src + d + (int64_t)P * j);
-#pragma unroll
-        for (int d = 0; d < P; ++d) dst[d * q + j] = v[d];
-    }
-}
+// The [q][P] <-> [P][q] transposes of the pack / unpack steps, tiled through shared
+// memory so both global sides are contiguous: a CTA owns JT consecutive j, i.e. one
+// contiguous run of JT*P interleaved elements and P runs of JT elements.  Shared slot
+// of (j, d): j*P + (d ^ (j & (P-1))) -- the XOR spreads the P values of one d over the
+// bank groups.
+constexpr int XL_THREADS = 256;
+constexpr int XL_ELEMS = 2048;   // elements per CTA tile (32 KiB)
 
-// dst[d + P*j] = src[d*q + j]  (the inverse)
-template <int P>
-__global__ void interleave_kernel(const double2 *__restrict__ src, double2 *__restrict__ dst, int64_t q) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < q; j += (int64_t)gridDim.x * blockDim.x) {
-        double2 v[P];
-#pragma unroll
-        for (int d = 0; d < P; ++d) v[d] = __ldg(src + d * q + j);
-#pragma unroll
-        for (int d = 0; d < P; ++d) dst[d + (int64_t)P * j] = v[d];
+// INTER = false: dst[d*q + j] = src[d + P*j] (deinterleave);  true: the inverse
+template <int P, bool INTER>
+__global__ void __launch_bounds__(XL_THREADS) xleave_kernel(const double2 *__restrict__ src,
+                                                             double2 *__restrict__ dst, int64_t q) {
+    constexpr int JT = XL_ELEMS / P;
+    __shared__ double2 tile[XL_ELEMS];
+    for (int64_t j0 = (int64_t)blockIdx.x * JT; j0 < q; j0 += (int64_t)gridDim.x * JT) {
+        const int jn = (int)((q - j0) < JT ? (q - j0) : JT);
+        if constexpr (!INTER) {
+            const double2 *s = src + P * j0;   // contiguous run of jn*P elements
+            for (int e = threadIdx.x; e < jn * P; e += XL_THREADS) {
+                const int j = e / P, d = e % P;
+                tile[j * P + (d ^ (j & (P - 1)))] = __ldg(s + e);
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < jn * P; e += XL_THREADS) {
+                const int d = e / jn, j = e % jn;
+                dst[d * q + j0 + j] = tile[j * P + (d ^ (j & (P - 1)))];
+            }
+        } else {
+            for (int e = threadIdx.x; e < jn * P; e += XL_THREADS) {
+                const int d = e / jn, j = e % jn;
+                tile[j * P + (d ^ (j & (P - 1)))] = __ldg(src + d * q + j0 + j);
+            }
+            __syncthreads();
+            double2 *o = dst + P * j0;
+            for (int e = threadIdx.x; e < jn * P; e += XL_THREADS) {
+                const int j = e / P, d = e % P;
+                o[e] = tile[j * P + (d ^ (j & (P - 1)))];
+            }
+        }
+        __syncthreads();
     }
 }
 
 static cudaError_t launch_xleave(bool inter, const double2 *src, double2 *dst, int p, int64_t q, cudaStream_t s) {
     if (q <= 0) return cudaSuccess;
-    int64_t blocks = (q + 255) / 256;
-    if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+    const int64_t jt = XL_ELEMS / p;
+    int64_t blocks = (q + jt - 1) / jt;
+    if (blocks > (int64_t)sm_count() * 6) blocks = (int64_t)sm_count() * 6;
 #define MOA_XL(PP)                                                                                   \
     case PP:                                                                                         \
-        if (inter) interleave_kernel<PP><<<(unsigned)blocks, 256, 0, s>>>(src, dst, q);              \
-        else deinterleave_kernel<PP><<<(unsigned)blocks, 256, 0, s>>>(src, dst, q);                  \
+        if (inter) xleave_kernel<PP, true><<<(unsigned)blocks, XL_THREADS, 0, s>>>(src, dst, q);     \
+        else xleave_kernel<PP, false><<<(unsigned)blocks, XL_THREADS, 0, s>>>(src, dst, q);          \
         break;
     switch (p) {
         MOA_XL(1)
