@@ -333,10 +333,9 @@ __device__ __forceinline__ double2 root_pi(uint32_t e, int t) {
 }
 
 // Build the tile's twiddle tables: omega^(al_t + be_t*(j + r*NB)) = A[t][j] * B[t][r],
-// by sincospi of the exact rational exponent (FP64 work, no loads: the two-level table
-// lookup was measured slower, its loads sit on the tile's critical path)
-// (computed at tile start from the plan's two-level omega_n table -- one product per
-// entry; the stages' barriers publish them).
+// each entry by sincospi of the exact rational exponent (FP64 work, no loads: a lookup in
+// the plan's two-level omega_n table was measured slower, its loads sit on the tile's
+// critical path); the stages' barriers publish the tables.
 template <int F, int T>
 __device__ __forceinline__ void build_twiddle_tables(const PassDesc &d, double2 *twa, double2 *twb, uint32_t al,
                                                      uint32_t be) {
