@@ -170,3 +170,22 @@ def test_binding_structs_match_the_header_layout(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(py), cname
         for f, _ in py._fields_:
             assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
+
+
+def test_c_client_compiles_links_and_runs(tmp_path):
+    """The header is a C99 header and the library links from plain C: gcc builds
+    tests/c/abi_host.c against include/moa_fft.h and libmoa_fft.so, and its host-only
+    checks (default lifting, a pass's index map, error codes + messages) pass on the CPU."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not on PATH")
+    moa.load()
+    exe = str(tmp_path / "abi_host")
+    libdir = os.path.dirname(moa.lib_path())
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c", "abi_host.c"), "-o", exe, moa.lib_path(),
+                        f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
