@@ -554,7 +554,7 @@ def test_size_2_29_sampled_bins_parseval_round_trip():
 
 def test_config_2_30_full_parity_elementwise():
     """BASELINE configs[3] on one GPU: n = 2^30 (16 GiB), default lifting
-    <32,32,256,256>, every one of the 2^30 outputs against the oracle (Fig 3.9)."""
+    <128,128,256,256>, every one of the 2^30 outputs against the oracle (Fig 3.9)."""
     t = 30
     x, ref = _big_case(t)
     xd = _device_copy(x)

@@ -125,7 +125,7 @@ def main():
         r["frac_survey"] = round(r["survey_GBps_cold"] / pk, 3)
         if t <= a.oracle_tmax:
             ot, cores = oracle_time(t)
-            r["oracle_s"], r["oracle_cores"] = (round(ot, 4), cores) if ot else (None, None)
+            r["oracle_s"], r["oracle_cores"] = (round(ot, 6), cores) if ot is not None else (None, None)
         rows.append(r)
         print(json.dumps(r), flush=True)
         torch.cuda.empty_cache()
@@ -146,7 +146,7 @@ def main():
             f.write("| t | lifting | launches | us (cold) | us (hot) | GFLOP/s (cold) | GFLOP/s (hot) | alg GB/s | "
                     "frac plan | frac survey | oracle s (cores) |\n|---|---|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
-                orc = f"{r['oracle_s']} ({r['oracle_cores']})" if r.get("oracle_s") else "-"
+                orc = f"{r['oracle_s']} ({r['oracle_cores']})" if r.get("oracle_s") is not None else "-"
                 f.write(f"| {r['t']} | {'x'.join(str(v) for v in r['lift'])} | {r['launches']} | {r['us_cold']} | "
                         f"{r['us_hot']} | {r['GFLOPs_cold']} | {r['GFLOPs_hot']} | {r['alg_GBps_cold']} | "
                         f"{r['frac_of_measured_hbm']} | {r['frac_survey']} | {orc} |\n")
