@@ -714,3 +714,48 @@ def test_tma_store_row_pass_bitwise_and_offsets(monkeypatch):
     assert oracle.rel_l2(ref[torch.from_numpy(ks).cuda()].cpu().numpy(),
                          oracle.dft_bins(x.cpu().numpy(), ks)) <= tol(t)
 
+
+
+def test_plan_execute_argument_checks():
+    """Plan.execute refuses tensors the C ABI would misread (wrong dtype, length, layout
+    or device) instead of reading out of bounds."""
+    n = 1 << 12
+    plan = moa.Plan(n)
+    good = torch.zeros(n, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="complex128"):
+        plan.execute(torch.zeros(n, dtype=torch.complex64, device="cuda"))
+    with pytest.raises(ValueError, match="elements"):
+        plan.execute(torch.zeros(n // 2, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError, match="contiguous"):
+        plan.execute(torch.zeros(2 * n, dtype=torch.complex128, device="cuda")[::2])
+    with pytest.raises(ValueError, match="cuda"):
+        plan.execute(torch.zeros(n, dtype=torch.complex128))
+    with pytest.raises(ValueError, match="elements"):
+        plan.execute(good, torch.empty(n + 1, dtype=torch.complex128, device="cuda"))
+    emu = moa.Plan(n, 4, -1, mode=moa.MODE_EMULATED)   # all 4 virtual ranks' slices: n elements
+    assert emu.expected_elems() == n
+    bat = moa.Plan(n, batch=3)
+    assert bat.expected_elems() == 3 * n
+    plan.execute(good)
+
+
+def test_bench_line_schema():
+    """bench.py on the GPU (small n): one JSON line with the contract's keys, the survey
+    and plan HBM fractions, a roofline block for the dominant kernel and the clocks."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--t", "20", "--steps", "5", "--warmup", "3",
+                        "--no-cpu"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "hbm"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["gpus_active"] == 1 and line["value"] > 0
+    assert line["roofline"]["bound"] == "hbm" and 0 < line["roofline"]["frac"] < 2
+    assert line["hbm"]["alg_bytes_survey"] == 32 * (1 << 20) * 2
+    assert line["e2e"]["h2d_bytes_per_step"] == 16 << 20 and line["e2e"]["d2h_bytes_per_step"] == 16 << 20
+    assert line["gpu_launches"] == 5 * 2
