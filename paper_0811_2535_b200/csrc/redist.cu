@@ -128,6 +128,7 @@ struct moa_redist_s {
     cudaStream_t stream = nullptr;
     double2 *S = nullptr, *R = nullptr;   // scratch (per virtual rank: S_r at S + r*s_elems)
     int64_t s_elems = 0, r_elems = 0;
+    int s_sets = 1, r_sets = 1;   // scratch sets allocated (p for per-rank scratch on virtual ranks)
     std::vector<Step> steps;
     int64_t messages = 0, bytes_max_rank = 0;
 };
@@ -142,8 +143,8 @@ static double2 *buf_of(moa_redist_s *pl, RBuf b, int r, const double2 *in, doubl
     switch (b) {
     case B_IN: return const_cast<double2 *>(in) + (pl->emulated ? vr * (pl->from == MOA_LAYOUT_CENTRAL ? 0 : pl->psize) : 0);
     case B_OUT: return out + (pl->emulated ? vr * (pl->to == MOA_LAYOUT_CENTRAL ? 0 : pl->psize) : 0);
-    case B_S: return pl->S + vr * pl->s_elems;
-    default: return pl->R + vr * pl->r_elems;
+    case B_S: return pl->S + (pl->s_sets > 1 ? vr : 0) * pl->s_elems;
+    default: return pl->R + (pl->r_sets > 1 ? vr : 0) * pl->r_elems;
     }
 }
 
@@ -313,12 +314,16 @@ moa_redist_t moa_redist_plan(int64_t n, int p, int from, int to, int route, int 
         delete pl;
         return nullptr;
     }
-    // scratch: real ranks hold one S/R each (rank 0 the n-element ones); emulated p sets
-    const int sets = pl->emulated ? p : 1;
-    const bool need_s = pl->s_elems > 0 && (pl->emulated || pl->s_elems < n || pl->rank == 0);
-    const bool need_r = pl->r_elems > 0 && (pl->emulated || pl->r_elems < n || pl->rank == 0);
-    if ((need_s && cudaMalloc((void **)&pl->S, (size_t)pl->s_elems * sets * sizeof(double2)) != cudaSuccess) ||
-        (need_r && cudaMalloc((void **)&pl->R, (size_t)pl->r_elems * sets * sizeof(double2)) != cudaSuccess)) {
+    // scratch: psize-element S/R on every rank for the direct block <-> cyclic routes (p sets
+    // on virtual ranks); the n-element ones of the central routes only on processor 0
+    const bool s_central = pl->s_elems == n, r_central = pl->r_elems == n;
+    const int s_sets = pl->emulated && !s_central ? p : 1, r_sets = pl->emulated && !r_central ? p : 1;
+    pl->s_sets = s_sets;
+    pl->r_sets = r_sets;
+    const bool need_s = pl->s_elems > 0 && (pl->emulated || !s_central || pl->rank == 0);
+    const bool need_r = pl->r_elems > 0 && (pl->emulated || !r_central || pl->rank == 0);
+    if ((need_s && cudaMalloc((void **)&pl->S, (size_t)pl->s_elems * s_sets * sizeof(double2)) != cudaSuccess) ||
+        (need_r && cudaMalloc((void **)&pl->R, (size_t)pl->r_elems * r_sets * sizeof(double2)) != cudaSuccess)) {
         cudaGetLastError();
         cudaFree(pl->S);
         delete pl;
