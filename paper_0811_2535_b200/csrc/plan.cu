@@ -212,6 +212,12 @@ int default_lifting(int tl, int64_t *lift, int p) {
         lift[2] = (int64_t)1 << (tl - 16);
         return 3;
     }
+    if (p > 1 && tl == 29) {   // <256, 512, 4096> (p > 1 keeps <= 3 levels): per rank of 2^30 over
+        lift[0] = 256;         // 2 virtual ranks 13.7 ms vs 21.0 ms as <8192, 256, 256>, 14.0 as
+        lift[1] = 512;         // <512, 256, 4096>, 15.1 as <512, 512, 2048> (tools/lift_p_probe.py)
+        lift[2] = 4096;
+        return 3;
+    }
     if (tl <= 27 || (p > 1 && tl <= 16 + FMAX_LOG)) {   // <2^(tl-16), 256, 256>
         lift[0] = (int64_t)1 << (tl - 16);
         lift[1] = 256;

@@ -572,21 +572,21 @@ def test_config_2_30_full_parity_elementwise():
     check_parts(num, den, t, "test_config_2_30_full_parity_elementwise")
 
 
-@pytest.mark.parametrize("exchange,chunks", [(moa.XCHG_NCCL, 8), (moa.XCHG_P2P, 0)])
-def test_config4_p8_exact_per_rank_plan(exchange, chunks):
+@pytest.mark.parametrize("P,exchange,chunks", [(8, moa.XCHG_NCCL, 8), (8, moa.XCHG_P2P, 0), (2, moa.XCHG_P2P, 0)])
+def test_config4_p8_exact_per_rank_plan(P, exchange, chunks):
     """BASELINE configs[3] partitioned p = 8 (8 x 2^27): the exact per-rank plan of the
     multi-GPU run -- local lifting <256, 256, 2048>, the weightcyclic twiddle + pack in the
     last pass, the all-to-all in G = 8 chunks (or the fused push, the bench's default
     exchange) and the P-point combine -- on 8 virtual ranks of one B200.  Rank r must
     hold X[r + 8 i] (the paper's xcyclic, Fig 5.8): every element of every rank
     against the oracle's slice."""
-    t, P = 30, 8
+    t = 30
     n = 1 << t
     x, ref = _big_case(t)
     xin = _device_copy(np.concatenate([x[r::P] for r in range(P)]))
     plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=exchange, chunks=chunks)
     info = plan.info()
-    assert info["lift"] == [256, 256, 2048] and info["local_n"] == 1 << 27
+    assert info["lift"] == ([256, 256, 2048] if P == 8 else [256, 512, 4096]) and info["local_n"] == n // P
     if exchange == moa.XCHG_NCCL:
         assert info["chunks"] == 8
     outd = plan.execute(xin)
@@ -602,7 +602,7 @@ def test_config4_p8_exact_per_rank_plan(exchange, chunks):
         a, b = parts_threads(got[r], ref[r::P])
         num += a
         den += b
-    check_parts(num, den, t, f"config4 p=8 emulated exchange={'p2p' if exchange else 'nccl G=8'}")
+    check_parts(num, den, t, f"2^30 p={P} emulated exchange={'p2p' if exchange else 'nccl G=8'}")
 
 
 def test_parity_harness_negative_control():

@@ -168,3 +168,5 @@ def test_default_lifting_table_every_t_and_p():
     assert moa.default_lifting(1 << 30) == [128, 128, 256, 256]
     assert moa.default_lifting(1 << 29) == [128, 128, 128, 256]
     assert moa.default_lifting(1 << 10) == [1024]
+    assert moa.default_lifting(1 << 30, 2) == [256, 512, 4096]   # per rank 2^29 (profiles/r02_lifting_recheck.md)
+    assert moa.default_lifting(1 << 30, 8) == [256, 256, 2048]   # configs[3]'s per-rank plan
