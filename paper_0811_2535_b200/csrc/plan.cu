@@ -218,6 +218,12 @@ int default_lifting(int tl, int64_t *lift, int p) {
         lift[2] = 4096;
         return 3;
     }
+    if (p > 1 && tl == 30) {   // <512, 512, 4096>: per rank of 2^31 over 2 virtual ranks 30.3 ms vs
+        lift[0] = 512;         // 32.8 as <1024, 1024, 1024>, 30.6 as <256, 1024, 4096>
+        lift[1] = 512;
+        lift[2] = 4096;
+        return 3;
+    }
     if (tl <= 27 || (p > 1 && tl <= 16 + FMAX_LOG)) {   // <2^(tl-16), 256, 256>
         lift[0] = (int64_t)1 << (tl - 16);
         lift[1] = 256;

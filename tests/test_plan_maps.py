@@ -170,3 +170,4 @@ def test_default_lifting_table_every_t_and_p():
     assert moa.default_lifting(1 << 10) == [1024]
     assert moa.default_lifting(1 << 30, 2) == [256, 512, 4096]   # per rank 2^29 (profiles/r02_lifting_recheck.md)
     assert moa.default_lifting(1 << 30, 8) == [256, 256, 2048]   # configs[3]'s per-rank plan
+    assert moa.default_lifting(1 << 31, 2) == [512, 512, 4096]
