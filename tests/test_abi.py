@@ -189,3 +189,23 @@ def test_c_client_compiles_links_and_runs(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,p,frm,to,route,mode,code,needle", [
+    (6, 2, 0, 1, 0, 2, -1, "2^t"),                 # n not a power of two (Fig 2.1)
+    (1 << 10, 3, 0, 1, 0, 2, -2, "power of two"),
+    (16, 8, 0, 1, 0, 2, -2, "psize"),              # psize < m
+    (1 << 10, 2, 0, 3, 0, 2, -9, "layout"),        # unknown layout
+    (1 << 10, 2, 0, 1, 2, 2, -9, "route"),         # unknown route
+    (1 << 10, 2, 0, 1, 0, 1, -9, "mode"),          # MOA_MODE_LITERAL is not a redistribution mode
+    (1 << 10, 2, 0, 1, 0, 0, -5, "moa_dist_init"), # real ranks without the communicator
+])
+def test_redist_plan_validation(n, p, frm, to, route, mode, code, needle):
+    """moa_redist_plan validates before it touches a GPU: NULL plus the
+    code and a message naming the violated bound."""
+    lib = moa.load()
+    assert not lib.moa_redist_plan(n, p, frm, to, route, mode)
+    assert lib.moa_fft_last_error_code() == code
+    assert needle in lib.moa_fft_last_error().decode()
+    assert lib.moa_redist_execute(None, None, None) == -9
+    lib.moa_redist_destroy(None)   # NULL-safe
