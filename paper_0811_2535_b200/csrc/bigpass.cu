@@ -20,10 +20,14 @@
 // Column tiles (middle pass, view [A][4096][B]) arrive by a 3-D bulk-tensor copy of
 // 16 boxes {2 columns, 256 points}; row tiles (last pass) by two 64 KiB bulk copies.
 // Each exchange runs in two rounds of 2048 positions per transform (X is half a tile):
-// exchange 1 splits positions by bit 3 ^ bit 11, exchange 2 by bit 7 ^ bit 11, so every
-// thread writes 8 and reads 8 values per round, and with the lane maps below the round
-// choice is uniform per warp.  Shared-memory addresses t*2048 + (q ^ swz(q) ^ 5t),
-// q = p mod 2048, are conflict-free for all four exchange accesses (tools/bank_sim_big.py).
+// exchange 1 splits positions by bit 3 ^ bit 11 (slot = p without bit 11), exchange 2 by
+// bit 4 ^ bit 8 (slot = p without bit 8), so every thread writes 8 and reads 8 values per
+// round -- the same 8 registers on both sides, with a warp-uniform round choice -- and
+// the addresses t*2048 + (q ^ swz(q) ^ 5t) are conflict-free for all four exchange
+// accesses (tools/bank_sim_big.py).
+//
+// Measured slower than three 256-point passes (2^24: 346 vs 260 µs; DESIGN.md §11,
+// profiles/r02_two_pass_2e24.md): compiled only into libmoa_fft_variants.so.
 #include "fft_pass.cuh"
 
 namespace moa {
