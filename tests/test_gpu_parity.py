@@ -759,3 +759,42 @@ def test_bench_line_schema():
     assert line["hbm"]["alg_bytes_survey"] == 32 * (1 << 20) * 2
     assert line["e2e"]["h2d_bytes_per_step"] == 16 << 20 and line["e2e"]["d2h_bytes_per_step"] == 16 << 20
     assert line["gpu_launches"] == 5 * 2
+
+
+def test_2_31_partitioned_consistent_with_single_gpu():
+    """n = 2^31 over 2 virtual ranks (per-rank lifting <512, 512, 4096>, the p > 1 default
+    at 2^30 per rank) against the single-GPU 2^31 transform, element by element: rank r's
+    output must be X[r::2] of the one-GPU result within the parity bar.  (A consistency
+    check between two CUDA paths, not an oracle comparison: the single-GPU 2^31 result is
+    pinned to the plain definition by test_max_size_2_31; the 2^30 per-rank plans are
+    pinned to the oracle element by element by test_config4_p8_exact_per_rank_plan.)"""
+    t, P = 31, 2
+    n = 1 << t
+    x = torch.empty(n, dtype=torch.complex128, device="cuda")
+    moa.gen_uniform(moa_inputs.seed_for(t), n, x)
+    single = moa.Plan(n).execute(x)
+    torch.cuda.synchronize()
+    ref = _host_copy(single)
+    del single
+    torch.cuda.empty_cache()
+    xin = torch.cat([x[r::P] for r in range(P)])
+    del x
+    torch.cuda.empty_cache()
+    plan = moa.Plan(n, P, -1, mode=moa.MODE_EMULATED, exchange=moa.XCHG_P2P)
+    assert plan.info()["lift"] == [512, 512, 4096]
+    outd = plan.execute(xin)
+    torch.cuda.synchronize()
+    plan.destroy()
+    del xin
+    got = _host_copy(outd).reshape(P, n // P)
+    del outd
+    torch.cuda.empty_cache()
+    from _parity import parts_threads, record
+    num = den = 0
+    for r in range(P):
+        a, b = parts_threads(got[r], ref[r::P])
+        num += a
+        den += b
+    err = float(np.sqrt(num / den))
+    record("2^31 p=2 emulated vs single GPU (consistency)", t, err)
+    assert err <= tol(t)
