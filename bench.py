@@ -285,7 +285,7 @@ def run_ours(args, rank: int, world: int):
     step_evs[-1].synchronize()
     step_ms = sorted(step_evs[i].elapsed_time(step_evs[i + 1]) for i in range(args.steps))
     step_stats = {"median": round(statistics.median(step_ms), 4), "min": round(step_ms[0], 4),
-                  "max": round(step_ms[-1], 4)}
+                  "mean": round(statistics.mean(step_ms), 4), "max": round(step_ms[-1], 4)}
 
     # ---- the same K steps again with an event pair around every kernel (moa_fft_set_profiling):
     # per-kernel durations for the roofline line
