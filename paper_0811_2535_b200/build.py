@@ -36,7 +36,9 @@ INST_LOGF = list(range(1, 14))
 
 
 def _sources_mtime() -> float:
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    # the product library does not depend on the variant-only sources
+    skip = set() if VARIANTS else {"fused.cu", "bigpass.cu"}
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f not in skip]
     files.append(os.path.join(ROOT, "include", "moa_fft.h"))
     files.append(os.path.abspath(__file__))
     return max(os.path.getmtime(f) for f in files)
