@@ -368,7 +368,7 @@ def run_ours(args, rank: int, world: int):
 
     if rank == 0:
         cpu = None
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:   # the oracle baseline: rank 0 at N = 1 only
             rate, cores, dt = cpu_oracle_rate(t, args.cpu_reps)
             cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{args.cpu_reps} full n=2^{t} oracle transforms ({dt:.2f} s each)",
@@ -487,7 +487,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--t", type=int, default=24)
-    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--cpu-reps", type=int, default=5,
+                    help="oracle transforms in the cpu_baseline sample (5 x 2^24 = about 11 s on 16 cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
