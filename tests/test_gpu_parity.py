@@ -647,8 +647,18 @@ def test_max_size_2_31():
     got = out[torch.from_numpy(ks).cuda()].cpu().numpy()
     win = 1 << 26
     ref = np.zeros(ks.size, dtype=np.complex128)
-    for j0 in range(0, n, win):
-        ref += oracle.dft_bins_range(x[j0:j0 + win].cpu().numpy(), n, j0, ks)
+    # the oracle side generates its own input windows from moa_inputs (never from the
+    # device) and sums the plain definition over them on all host cores
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    def part(j0):
+        xw = moa_inputs.complex_signal(moa_inputs.seed_for(t), win, first=j0)
+        return oracle.dft_bins_range(xw, n, j0, ks)
+
+    with ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
+        for v in ex.map(part, range(0, n, win)):
+            ref += v
     check(got, ref, t, "test_max_size_2_31")
     lhs = sum(torch.sum(out[j0:j0 + win].abs() ** 2).item() for j0 in range(0, n, win))
     rhs = n * sum(torch.sum(x[j0:j0 + win].abs() ** 2).item() for j0 in range(0, n, win))
@@ -711,8 +721,8 @@ def test_tma_store_row_pass_bitwise_and_offsets(monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(y, ref)
     ks = np.array([0, 1, 12345, n // 2 + 3, n - 1])
-    assert oracle.rel_l2(ref[torch.from_numpy(ks).cuda()].cpu().numpy(),
-                         oracle.dft_bins(x.cpu().numpy(), ks)) <= tol(t)
+    check(ref[torch.from_numpy(ks).cuda()].cpu().numpy(),
+          oracle.dft_bins(moa_inputs.signal_for(t), ks), t, "TMA-store row pass, sampled bins")
 
 
 
@@ -767,16 +777,16 @@ def test_2_31_partitioned_consistent_with_single_gpu():
     output must be X[r::2] of the one-GPU result within the parity bar.  (A consistency
     check between two CUDA paths, not an oracle comparison: the single-GPU 2^31 result is
     pinned to the plain definition by test_max_size_2_31; the 2^30 per-rank plans are
-    pinned to the oracle element by element by test_config4_p8_exact_per_rank_plan.)"""
+    pinned to the oracle element by element by test_config4_p8_exact_per_rank_plan.)
+    Compared on the device in chunks (float64 sums) to keep the 64 GiB off the host."""
     t, P = 31, 2
     n = 1 << t
     x = torch.empty(n, dtype=torch.complex128, device="cuda")
     moa.gen_uniform(moa_inputs.seed_for(t), n, x)
-    single = moa.Plan(n).execute(x)
+    plan1 = moa.Plan(n)
+    single = plan1.execute(x)
     torch.cuda.synchronize()
-    ref = _host_copy(single)
-    del single
-    torch.cuda.empty_cache()
+    plan1.destroy()
     xin = torch.cat([x[r::P] for r in range(P)])
     del x
     torch.cuda.empty_cache()
@@ -786,15 +796,19 @@ def test_2_31_partitioned_consistent_with_single_gpu():
     torch.cuda.synchronize()
     plan.destroy()
     del xin
-    got = _host_copy(outd).reshape(P, n // P)
-    del outd
     torch.cuda.empty_cache()
-    from _parity import parts_threads, record
-    num = den = 0
+    M = n // P
+    num = den = 0.0
+    step = 1 << 26
     for r in range(P):
-        a, b = parts_threads(got[r], ref[r::P])
-        num += a
-        den += b
+        for s0 in range(0, M, step):
+            g = outd[r * M + s0:r * M + s0 + step]
+            o = single[r + P * s0:r + P * (s0 + step):P]
+            num += torch.sum((g - o).abs() ** 2).item()
+            den += torch.sum(o.abs() ** 2).item()
+    del outd, single
+    torch.cuda.empty_cache()
+    from _parity import record
     err = float(np.sqrt(num / den))
     record("2^31 p=2 emulated vs single GPU (consistency)", t, err)
     assert err <= tol(t)
