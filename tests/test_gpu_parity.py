@@ -812,3 +812,30 @@ def test_2_31_partitioned_consistent_with_single_gpu():
     err = float(np.sqrt(num / den))
     record("2^31 p=2 emulated vs single GPU (consistency)", t, err)
     assert err <= tol(t)
+
+
+def test_concurrent_plans_on_separate_streams():
+    """Plans are independent objects ordered on their own streams: two plans of different
+    sizes executing concurrently on two streams (and a third reusing a destroyed plan's
+    sizes) each equal the oracle; graph replay follows the (in, out) pointers per plan."""
+    ta, tb = 20, 16
+    xa, xb = moa_inputs.signal_for(ta), moa_inputs.signal_for(tb)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    pa, pb = moa.Plan(1 << ta, stream=sa), moa.Plan(1 << tb, stream=sb)
+    da, db = _dev(xa), _dev(xb)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(sa):
+        oa = torch.empty_like(da)
+    with torch.cuda.stream(sb):
+        ob = torch.empty_like(db)
+    for _ in range(3):
+        pa.execute(da, oa)
+        pb.execute(db, ob)
+    torch.cuda.synchronize()
+    check(oa.cpu().numpy(), oracle.fft(xa, -1, threads=8), ta, "concurrent plans (stream a)")
+    check(ob.cpu().numpy(), oracle.fft(xb, -1, threads=8), tb, "concurrent plans (stream b)")
+    pa.destroy()
+    pc = moa.Plan(1 << ta, stream=sb)
+    oc = pc.execute(da)
+    torch.cuda.synchronize()
+    assert torch.equal(oc, oa)
