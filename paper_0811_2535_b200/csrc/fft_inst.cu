@@ -71,6 +71,8 @@ cudaError_t MOA_CAT(launch_pass_tma_f, MOA_INST_LOGF)(int T, int src, const Pass
             if (src == 2) return launch_one_tma<kF, TT, 2>(d, map, tiles, grid, s);        \
             if (src == 4) return launch_one_tpf<kF, TT, 4>(d, map, tiles, grid, s);        \
             if (src == 5) return launch_one_tpf<kF, TT, 5>(d, map, tiles, grid, s);        \
+            if (src == 6) return launch_one_tma1<kF, TT, 6>(d, map, tiles, s);             \
+            if (src == 7) return launch_one_tma1<kF, TT, 7>(d, map, tiles, s);             \
         }                                                                                  \
         return cudaErrorInvalidValue;                                                      \
     }
@@ -93,6 +95,7 @@ int MOA_CAT(grid_pass_tma_f, MOA_INST_LOGF)(int T, int src) {
             if (src == 2) return grid_one_tma<kF, TT, 2>();             \
             if (src == 4) return grid_one_tpf<kF, TT, 4>();             \
             if (src == 5) return grid_one_tpf<kF, TT, 5>();             \
+            if (src == 6 || src == 7) return 1;                         \
         }                                                               \
         return 0;                                                       \
     }

@@ -1039,6 +1039,58 @@ __global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Non-persistent TMA-loaded pass (SRC 6 = column tile, 7 = row tile): the plain pass's
+// one tile per CTA, but the tile arrives as ONE bulk-tensor copy issued by one thread
+// (box {2T doubles, 256 points} or row boxes) into the exchange buffer under an
+// mbarrier instead of 16 LDG.128 per thread; the first stage reads it from shared memory
+// and the buffer becomes the exchange buffer.  Same shared memory and occupancy as
+// fft_pass_kernel.
+template <int F, int T, int SRC>
+__global__ void __launch_bounds__(PassShape<F, T>::NT, PassShape<F, T>::MINB)
+    fft_pass_tma1_kernel(const PassDesc d, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int SL = SRC == 6 ? 1 : 2;
+    using SH = TpfShape<F, T, SL + 3>;
+    extern __shared__ unsigned char smraw[];
+    unsigned char *base = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
+    double2 *buf = reinterpret_cast<double2 *>(base);
+    double2 *tw = reinterpret_cast<double2 *>(base + SH::BUF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + SH::BUF + SH::TW);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    if (d.pdl) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tma_issue_tile<F, T, SL>(&tmap, bar, buf, d, blockIdx.x);
+    const TileIO io{d.src, d.dst, d.in_shift, d.out_shift};
+    mbar_wait(bar, 0);
+    tile_fft<F, T, SL, SyncHook>(buf, tw, d, io, blockIdx.x, buf, SyncHook());
+}
+
+template <int F, int T, int SRC>
+cudaError_t launch_one_tma1(const PassDesc &d, const CUtensorMap &map, int64_t tiles, cudaStream_t s) {
+    using SH = TpfShape<F, T, (SRC == 6 ? 1 : 2) + 3>;
+    static_assert(SH::SMEM <= 227 * 1024, "smem");
+    if (SH::SMEM > 48 * 1024)
+        cudaFuncSetAttribute(fft_pass_tma1_kernel<F, T, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SH::SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tiles);
+    cfg.blockDim = dim3(PassShape<F, T>::NT);
+    cfg.dynamicSmemBytes = SH::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = d.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fft_pass_tma1_kernel<F, T, SRC>, d, map);
+}
+
 template <int F, int T, int SRC>
 cudaError_t launch_one_tpf(const PassDesc &d, const CUtensorMap &map, int64_t tiles, int grid, cudaStream_t s) {
     fft_pass_tpf_kernel<F, T, SRC><<<grid, PassShape<F, T>::NT, TpfShape<F, T, SRC>::SMEM, s>>>(d, map, tiles);

@@ -99,7 +99,7 @@ int encode_pass_map(PassPlan &pp, const void *base) {
     cuuint64_t dims[4], strides[3];
     cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
     cuuint32_t rank;
-    if (pp.tma == 1 || pp.tma == 4 || (pp.big && !pp.d.last)) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
+    if (pp.tma == 1 || pp.tma == 4 || pp.tma == 6 || (pp.big && !pp.d.last)) {   // column tile of the view [A][F][B]: dims {2B doubles, F, A}
         const uint64_t B = (uint64_t)D.in_f, A = (uint64_t)D.V;
         rank = 3;
         dims[0] = 2 * B;
@@ -171,11 +171,13 @@ void choose_tma(PassPlan &pp) {
     if (!D.last && D.in_t == 1 && pp.T >= 2) src = 1;
     else if (D.last && D.in_f == 1) src = 2;
     if (!src) return;
-    const int code = tma_kind == 2 ? src + 3 : src;
+    // 1: persistent double-buffered, 2: persistent single buffer + prefetch (src 4/5),
+    // 3: one tile per CTA loaded by one bulk-tensor copy (src 6/7, fft_pass_tma1_kernel)
+    const int code = tma_kind == 2 ? src + 3 : (tma_kind == 3 ? src + 5 : src);
     int g = pass_tma_grid(pp.logF, pp.T, code);
     if (g <= 0) return;
     pp.tma = code;
-    pp.tma_grid = g;
+    pp.tma_grid = code >= 6 ? (int)pp.tiles : g;
 #endif
 }
 
