@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "complex128 1-D FFT GFLOP/s (5n log2 n) and HBM GB/s fraction, 1/2/4/8 B200"
 UNIT = "GFLOP/s"
+L2_BYTES = 126 * 1000 * 1000   # B200 L2 (B200_PROFILING.md)
 
 
 def flops(n: int) -> float:
@@ -168,23 +169,24 @@ def run_reference(args, rank: int, world: int):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(t, world, None),
+            "config": config_block(t, world, None, l2_flush=16 * (n // world) < 2 * L2_BYTES),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_block(t: int, world: int, info, exchange: str = "nccl"):
+def config_block(t: int, world: int, info, exchange: str = "nccl", l2_flush: bool = False):
     c = {"workload": f"fft1d_c2c_forward_n2^{t}", "n": 1 << t, "p": world,
          "input": "i.i.d. uniform [-1,1) re/im, SplitMix64 seed 0x08112535+t",
          "parallelism": ((f"reshape-transpose p={world} (" + ("fused NVLink push + 8 B NCCL barrier"
                                                               if exchange == "p2p" else "NCCL all-to-all")
                           + ")") if world > 1 else "single GPU"),
-         "l2": "working set (in + out + scratch = 768 MiB at 2^24) larger than the 126 MB L2; no flush"}
-    if info is not None:
-        c["lift"] = info["lift"]
-        c["passes"] = info["passes"]
+         "l2": (f"rank input of 16 n/p = {16 * (1 << t) / world / 2**20:.1f} MiB is not clearly larger than the 126 MB "
+                "L2: a 512 MiB L2 flush (outside the timed events) before every timed step, step times summed")
+               if l2_flush else
+               (f"working set (in + out + scratch = {3 * 16 * (1 << t) // world >> 20} MiB per rank) larger than "
+                "the 126 MB L2; no flush, K steps back to back in one event pair")}
     return c
 
 
@@ -259,20 +261,42 @@ def run_ours(args, rank: int, world: int):
     # sits between the kernels here: an event between two launches would serialise the
     # programmatic dependent launch the passes use (the next pass's CTAs are scheduled
     # while the previous pass drains).
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # When this rank's input is not clearly larger than the 126 MB L2 (p > 1: 2^24 / p), the
+    # L2 is flushed (a 512 MiB write, outside the event pair) before every timed step and
+    # the step times are summed; otherwise the K steps run back to back in one event pair.
+    flush = 16 * M < 2 * L2_BYTES
     sampler = ClockSampler(dev.index)
     barrier()
     torch.cuda.synchronize()
-    with sampler:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            plan.execute(x, out)
-        ev1.record(stream)
-        ev1.synchronize()
-    torch.cuda.synchronize()
-    barrier()
-    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    if flush:
+        fl = torch.empty(1 << 27, dtype=torch.float32, device=dev)
+        pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+        with sampler:
+            with torch.cuda.stream(stream):
+                for a, b in pairs:
+                    fl.fill_(1.0)
+                    a.record(stream)
+                    plan.execute(x, out)
+                    b.record(stream)
+            pairs[-1][1].synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        elapsed = sum(a.elapsed_time(b) for a, b in pairs) * 1e-3
+        del fl
+    else:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with sampler:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                plan.execute(x, out)
+            ev1.record(stream)
+            ev1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        elapsed = ev0.elapsed_time(ev1) * 1e-3
+    args.l2_flush = flush
 
     # ---- per-step spread (median / min / max) from K more steps with an event between steps
     step_evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -394,7 +418,9 @@ def run_ours(args, rank: int, world: int):
                 "gpus_active": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_block(t, world, info, args.exchange),
+                "config": config_block(t, world, info, args.exchange, getattr(args, "l2_flush", False)),
+                "plan": {"lift": info["lift"], "passes": info["passes"], "chunks": info["chunks"],
+                         "exchange": args.exchange if world > 1 else None},
                 "hbm": hbm,
                 "roofline": roofline, "kernels": kstats, "cpu_baseline": cpu, "e2e": e2e,
                 "plan_ms": round(plan_ms, 2), "step_ms": step_stats,
