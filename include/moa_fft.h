@@ -176,7 +176,9 @@ moa_fft_plan_t moa_fft_plan_ex(int64_t n, int p, int sign, const moa_fft_options
  * stream) and launches it; the graph only remembers the pointer values, so the
  * caller may free or reuse the buffers afterwards.  (Tuning knobs: every MOA_FFT_*
  * environment variable -- e.g. MOA_FFT_GRAPH=0 -- is ignored unless MOA_FFT_ABLATION=1.)
- * Returns MOA_OK or MOA_ERR_ALIGN / MOA_ERR_CUDA / MOA_ERR_NCCL.
+ * in and out are either the same pointer or disjoint ranges (a partial overlap is
+ * MOA_ERR_INVALID_ARG).
+ * Returns MOA_OK or MOA_ERR_ALIGN / MOA_ERR_INVALID_ARG / MOA_ERR_CUDA / MOA_ERR_NCCL.
  */
 int moa_fft_execute(moa_fft_plan_t plan, const void *in, void *out);
 

@@ -39,6 +39,12 @@ int moa_fft_execute(moa_fft_plan_t pl, const void *in, void *out) {
     if (!pl) return fail(MOA_ERR_INVALID_ARG, "NULL plan");
     if (!aligned16(in) || !aligned16(out))
         return fail(MOA_ERR_ALIGN, "in/out must be non-NULL 16-byte aligned device pointers");
+    {   // in == out (in place) or disjoint: a partial overlap would be read after being written
+        const int64_t elems = pl->rows ? pl->n : (pl->mode == MOA_MODE_EMULATED ? pl->n : pl->M * pl->batch);
+        const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out, len = (uintptr_t)elems * 16u;
+        if (a != b && a < b + len && b < a + len)
+            return fail(MOA_ERR_INVALID_ARG, "in and out overlap without being equal (in place needs in == out)");
+    }
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != pl->device) cudaSetDevice(pl->device);

@@ -839,3 +839,17 @@ def test_concurrent_plans_on_separate_streams():
     oc = pc.execute(da)
     torch.cuda.synchronize()
     assert torch.equal(oc, oa)
+
+
+def test_partial_overlap_rejected():
+    """in == out (in place) or disjoint: a partially overlapping out is refused by the ABI."""
+    n = 1 << 12
+    buf = torch.zeros(2 * n, dtype=torch.complex128, device="cuda")
+    plan = moa.Plan(n)
+    lib = moa.load()
+    base = buf.data_ptr()
+    assert lib.moa_fft_execute(plan._h, base, base + 16 * 8) == -9
+    assert lib.moa_fft_last_error_code() == -9
+    assert lib.moa_fft_execute(plan._h, base, base + 16 * n) == 0     # adjacent, disjoint
+    assert lib.moa_fft_execute(plan._h, base, base) == 0              # in place
+    torch.cuda.synchronize()
