@@ -470,6 +470,24 @@ def a2a_diagnostic(moa, n, world, stream, x, steps, kstats_main, step_s, dev):
                         dtype=torch.float64, device=dev)
     dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_a2a, t_p1, t_comb, t_push_extra = [float(v) for v in vals.tolist()]
+    # reference: torch's own NCCL all_to_all_single on the same per-peer size (16 M / p bytes
+    # per ordered pair), timed the same way -- the "measured NCCL all-to-all peak" of §8(d)
+    sbuf = torch.empty(2 * M, dtype=torch.float64, device=dev)
+    rbuf = torch.empty_like(sbuf)
+    for _ in range(3):
+        dist.all_to_all_single(rbuf, sbuf)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ra, rb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ra.record()
+    for _ in range(steps):
+        dist.all_to_all_single(rbuf, sbuf)
+    rb.record()
+    rb.synchronize()
+    t_ref = torch.tensor([ra.elapsed_time(rb) * 1e-3 / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t_ref, op=dist.ReduceOp.MAX)
+    t_ref = float(t_ref.item())
+    del sbuf, rbuf
     alg = 16.0 * M / t_a2a / 1e9 if t_a2a > 0 else None
     bus = alg * (world - 1) / world if alg else None
     res = {"t_a2a_us": round(t_a2a * 1e6, 2), "t_phase1_us": round(t_p1 * 1e6, 2),
@@ -477,6 +495,8 @@ def a2a_diagnostic(moa, n, world, stream, x, steps, kstats_main, step_s, dev):
            "algBw_GBps": round(alg, 1) if alg else None, "busBw_GBps": round(bus, 1) if bus else None,
            "busBw_frac_of_900": round(bus / 900.0, 4) if bus else None,
            "busBw_frac_of_770_measured": round(bus / 770.0, 4) if bus else None,
+           "nccl_a2a_ref_us": round(t_ref * 1e6, 2),
+           "frac_of_nccl_a2a_ref": round(t_ref / t_a2a, 4) if t_a2a > 0 else None,
            "overlap_efficiency": round((t_p1 + t_a2a + t_comb - step_s) / min(t_a2a, t_p1 + t_comb), 4)
            if t_a2a > 0 else None,
            "how": "unchunked NCCL plan, events around every launch on the plan stream, max over ranks"}
