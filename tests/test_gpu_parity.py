@@ -528,6 +528,20 @@ def test_large_sizes_full_parity_elementwise(t):
     check_parts(num, den, t, "test_large_sizes_full_parity_elementwise")
 
 
+def test_sign_plus_one_large_elementwise():
+    """The paper's literal exponent EXP(+2 pi i ...) (sign +1; computed as
+    conj(FFT_-1(conj x))) at 2^26, where every pass is HBM-resident: every element against
+    the oracle run with sign +1."""
+    t = 26
+    x = moa_inputs.complex_signal_threads(moa_inputs.seed_for(t), 1 << t)
+    ref = oracle.fft(x, +1, threads=oracle.max_threads())
+    got = _host_copy(moa.Plan(1 << t, 1, +1).execute(_device_copy(x)))
+    torch.cuda.empty_cache()
+    from _parity import parts_threads
+    num, den = parts_threads(got, ref)
+    check_parts(num, den, t, "sign +1 at 2^26")
+
+
 def test_size_2_29_sampled_bins_parseval_round_trip():
     """2^29 (<128,128,128,256>): sampled bins against the plain definition (long double),
     Parseval on the whole output, and the device round trip FFT_+1(FFT_-1 x)/n = x."""
