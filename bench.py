@@ -215,24 +215,44 @@ def run_ours(args, rank: int, world: int):
     if world > 1 and args.exchange in ("p2p", "auto"):
         # the fused NVLink exchange, admitted only if every rank reproduces the NCCL
         # path's result bit for bit (same arithmetic, only the transport differs)
+        # every step that contains a collective runs only once all ranks agree the previous
+        # one succeeded, so a failure on one rank cannot leave the others blocked in NCCL
+        def agree(ok_local: int) -> bool:
+            f = torch.tensor([ok_local], dtype=torch.int32, device=dev)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            return int(f.item()) == 1
+
+        cand = None
         ok = 1
         try:
-            cand = moa.Plan(n, world, -1, stream=stream, exchange=moa.XCHG_P2P)
-            cand.enable_p2p()
-            ref_plan = moa.Plan(n, world, -1, stream=stream)
-            with torch.cuda.stream(stream):
-                a = cand.execute(x)
-                b = ref_plan.execute(x)
-            stream.synchronize()
-            ok = int(torch.equal(a, b))
-            ref_plan.destroy()
-            del a, b
+            cand = moa.Plan(n, world, -1, stream=stream, exchange=moa.XCHG_P2P)   # collective-free
         except Exception as e:  # noqa: BLE001 - any failure falls back to NCCL
-            print(f"p2p exchange unavailable ({e}); using NCCL", file=sys.stderr)
-            ok, cand = 0, None
-        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 1:
+            print(f"p2p plan unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+        if agree(ok):
+            try:
+                cand.enable_p2p()                      # collective: handle all-gather
+            except Exception as e:  # noqa: BLE001
+                print(f"p2p mapping failed ({e}); using NCCL", file=sys.stderr)
+                ok = 0
+        else:
+            ok = 0
+        if agree(ok):
+            try:
+                ref_plan = moa.Plan(n, world, -1, stream=stream)
+                with torch.cuda.stream(stream):
+                    a = cand.execute(x)
+                    b = ref_plan.execute(x)
+                stream.synchronize()
+                ok = int(torch.equal(a, b))
+                ref_plan.destroy()
+                del a, b
+            except Exception as e:  # noqa: BLE001
+                print(f"p2p exchange check failed ({e}); using NCCL", file=sys.stderr)
+                ok = 0
+        else:
+            ok = 0
+        if agree(ok):
             plan = cand
         else:
             if args.exchange == "p2p":
