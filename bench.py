@@ -465,7 +465,17 @@ def a2a_diagnostic(moa, n, world, stream, x, steps, kstats_main, step_s, dev):
     import torch
     import torch.distributed as dist
     M = n // world
-    diag = moa.Plan(n, world, -1, stream=stream, chunks=1)
+    ok = 1
+    try:
+        diag = moa.Plan(n, world, -1, stream=stream, chunks=1)
+    except Exception:  # noqa: BLE001 - agree before any collective below
+        ok = 0
+    f = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(f, op=dist.ReduceOp.MIN)
+    if int(f.item()) != 1:
+        if ok:
+            diag.destroy()
+        return {"error": "diagnostic plan creation failed on some rank"}
     out = torch.empty_like(x)
     with torch.cuda.stream(stream):
         for _ in range(2):
